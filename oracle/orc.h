@@ -1,0 +1,138 @@
+/*
+ * orc.h -- CPU ORACLE for the GS-Cache per-frame hot path (TEST INFRASTRUCTURE).
+ *
+ * This is test infrastructure, not product code.  Only tests/, the smoke()
+ * entry of __graft_entry__.py and bench.py's cpu_baseline / --impl reference
+ * legs may load it.  It shares no code with paper_2502_14938_b200/ (no common
+ * headers, helpers, tables or constants); both sides read the same GSC2 scene
+ * and trajectory produced by scenegen/.
+ *
+ * It is a plain, slow, step-by-step implementation of SURVEY.md §8(c)
+ * (O-0 .. O-8), in the paper's order:
+ *   binocular unify (Eqs. 5-6) -> anchor filtering + LoD
+ *   (Alg. 1) -> cache state machine with explicit eviction
+ *   (Alg. 1, Eq. 4) -> derivation of misses through the
+ *   opacity / colour / covariance MLPs (Eq. 3, Eq. 2)
+ *   -> EWA projection with opacity-aware extent and exact tile coverage
+ *    -> (tile, depth) key duplication + sort -> per-tile
+ *   front-to-back blending (Eq. 1, Alg. 1), both eyes.
+ *
+ * Every fp32 expression follows DESIGN.md "Numerics" op by op (no FMA except
+ * the fmaf() Horner steps of the elementary functions); build with
+ * -ffp-contract=off -fno-fast-math.
+ */
+#ifndef GSC_ORACLE_H
+#define GSC_ORACLE_H
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define ORC_F 32
+#define ORC_K 10
+#define ORC_H 32
+#define ORC_NOUT (ORC_K * 11)
+
+typedef struct {
+  int N, L;
+  float d0;
+  const float *pos;      /* [N*3] */
+  const int8_t *feat;    /* [N*F] */
+  const float *offs;     /* [N*K*3] */
+  const float *scale;    /* [N*3] */
+  const uint8_t *level;  /* [N] */
+  const int8_t *W1, *b1, *W2a, *b2a, *W2c, *b2c, *W2s, *b2s;
+} orc_scene;
+
+typedef struct {
+  int width, height;
+  double fov_y, near_plane, far_plane;
+  float bg[3];
+  int d_max;
+  int depth_literal; /* 1: SPEC-literal H(miss rate); 0: H(novelty) */
+} orc_config;
+
+typedef struct { double p[3]; double q[4]; } orc_eye;
+
+typedef struct {
+  float p[3], r0[3], r1[3], r2[3];
+  float fx, fy, cx, cy, near_plane, far_plane, limx, limy;
+} orc_eye_consts;
+
+typedef struct {
+  float p[3], right[3], up[3], fwd[3];
+  float near_plane, far_plane, tx, ty, kx, ky;
+  double p64[3], fwd64[3], up64[3], pullback64;
+} orc_unified;
+
+typedef struct {
+  float u, v, A, B, C, alpha, rgb[3];
+  float depth, thr;
+  int tx0, tx1, ty0, ty1; /* candidate tile box, inclusive; tx0 > tx1 => empty */
+  int ntiles;             /* kept tiles */
+} orc_splat;
+
+typedef struct {
+  /* counts */
+  int64_t frame;
+  int n_visible, n_hits, n_misses, n_new, n_live, depth_used, depth_next;
+  int64_t n_splats[2], n_pairs[2];
+  int64_t n_evals; /* per-pixel splat evaluations in the blend */
+} orc_frame_stats;
+
+/* ---- elementary functions (DESIGN.md Numerics E1-E4) ---- */
+float orc_exp_s(float x);
+float orc_log_s(float x);
+float orc_tanh_s(float x);
+float orc_sigmoid_s(float x);
+void orc_elem_vec(int fn, const float *in, float *out, size_t n); /* fn: 0 exp 1 log 2 tanh 3 sigmoid */
+
+/* ---- cameras (Eqs. 5-6) ---- */
+int orc_eye_constants(const orc_config *cfg, const orc_eye *e, orc_eye_consts *out);
+int orc_unify(const orc_config *cfg, const orc_eye *l, const orc_eye *r, orc_unified *out);
+
+/* ---- per-element steps ---- */
+float orc_margin(const float *offs_i, const float *s_i);
+int orc_lod_cut(const orc_unified *u, int L, float d0, const float *p);
+int orc_visible(const orc_unified *u, int L, float d0, const float *p, float margin, int level);
+void orc_build_cov(const float q[4], const float S[3], float cov[6]);
+void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alpha, float *mu,
+                       float *cov, float *rgb, float *o_raw /* [110] or NULL */);
+int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, const float *mu,
+                const float *cov, const float *rgb, orc_splat *out);
+int orc_tile_kept(const orc_config *cfg, const orc_splat *s, int tx, int ty);
+float orc_tile_qmin(const orc_config *cfg, const orc_splat *s, int tx, int ty);
+void orc_blend_pixel(const orc_splat *const *list, int n, float px_center_x, float px_center_y,
+                     const float bg[3], float out[3], float *T_out, int *n_eval);
+int orc_depth_H(int d_max, int64_t num, int64_t den);
+
+/* ---- whole frames ---- */
+typedef struct orc_state orc_state;
+orc_state *orc_create(const orc_scene *sc, const orc_config *cfg);
+void orc_destroy(orc_state *st);
+void orc_reset(orc_state *st);
+
+#define ORC_RASTER 1u   /* project + sort + blend (else cache state machine only) */
+#define ORC_BRUTE  2u   /* O1 per-pixel brute force instead of the tiled O2 renderer */
+
+/* outputs are optional (NULL to skip); img_* are planar [3][H][W] */
+int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
+              orc_frame_stats *stats, float *img_l, float *img_r);
+
+/* state / intermediate access after orc_frame (valid until the next call) */
+int orc_get_visible(const orc_state *st, uint32_t *dst, int cap);
+int orc_get_misses(const orc_state *st, uint32_t *dst, int cap);
+int32_t orc_get_birth(const orc_state *st, int i);
+void orc_get_pool(const orc_state *st, int64_t slot0, int64_t count, float *alpha, float *mu,
+                  float *cov, float *rgb);
+int64_t orc_get_pairs(const orc_state *st, uint64_t *keys, uint32_t *gs, int64_t cap);
+int64_t orc_get_splats(const orc_state *st, int eye, uint32_t *gs, float *rec /* [n][12] */, int64_t cap);
+int orc_num_threads(void);
+void orc_set_threads(int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif
