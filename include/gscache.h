@@ -1,0 +1,180 @@
+/*
+ * gscache.h -- C ABI of the B200-native GS-Cache per-frame hot path.
+ *
+ * The calls follow the paper's problem statement: load a trained
+ * structured-3DGS scene, feed the binocular HMD pose of each
+ * frame ("each frame ... contains two poses of the binocular stereo cameras",
+ * P:310) and get the two eye images.  One render call runs, on the
+ * GPU, SURVEY.md §8(a) rows a1..a8:
+ *   a0 unified camera (Eqs. 5-6; host fp64 -> fp32 constants)
+ *   a1 frustum + LoD anchor culling and cache classify (Alg. 1)
+ *   a2 cache-depth policy + watermark (Eq. 4, Alg. 1)
+ *   a3 derivation of cache misses through the opacity / colour / covariance
+ *      MLPs into the persistent Gaussian pool (Eq. 3)
+ *   a4 EWA projection, opacity-aware extent, exact tile count
+ *   a5 depth sort + (tile, depth) key duplication
+ *   a6 radix sort by tile (onesweep LSD; with a5 this is the (tile, depth) sort)
+ *   a7 per-tile ranges
+ *   a8 per-tile front-to-back blending for both eyes (Eq. 1, Alg. 1)
+ *
+ * Conventions
+ *  - Every call returns gsc_status; no C++ exception crosses the ABI.
+ *  - Errors are sticky per context only for GSC_ECUDA (destroy the context).
+ *    gsc_last_error() returns a NUL-terminated description of the last error.
+ *  - A context owns all device memory it allocates (scene SoA, Gaussian pool,
+ *    cache state, sort / splat buffers).  Output image buffers and CUDA
+ *    streams belong to the caller.  One context = one rendering worker with a
+ *    private cache; distinct contexts are independent; a context
+ *    must not be used from two threads at once.
+ *  - Camera convention: q = (w,x,y,z) unit quaternion,
+ *    world-from-camera; camera right = R[:,0], up = R[:,1], forward = -R[:,2].
+ *  - Images: GSC_FMT_RGB_F32_PLANAR = float[3][H][W] (12*W*H bytes),
+ *    GSC_FMT_RGBA8 = uint8[H][W][4] (4*W*H bytes, alpha = 255*(1-T)).
+ */
+#ifndef GSCACHE_H
+#define GSCACHE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GSC_ABI_VERSION 1
+
+typedef enum {
+  GSC_OK = 0,
+  GSC_EINVAL = 1,      /* invalid argument */
+  GSC_EFORMAT = 2,     /* malformed scene file; byte offset in gsc_last_error */
+  GSC_EDEGENERATE = 3, /* antiparallel eye directions */
+  GSC_ENOMEM = 4,      /* device or pinned allocation failed */
+  GSC_ECUDA = 5,       /* CUDA runtime error; sticky */
+  GSC_EINTERNAL = 6,   /* internal consistency failure */
+  GSC_ESTATE = 7,      /* call out of order (render before load/pose) */
+  GSC_ECAPACITY = 8    /* a frame produced more (tile, depth) pairs than pair_capacity */
+} gsc_status;
+
+typedef struct gsc_ctx gsc_ctx;
+
+/* flags */
+#define GSC_F_DEPTH_LITERAL 0x1u /* SPEC-literal H(miss rate) instead of H(novelty) */
+#define GSC_F_STAGE_TIMING 0x2u  /* record CUDA events between the stages of every frame */
+
+typedef struct {
+  int width, height;        /* pixels per eye */
+  double fov_y;             /* vertical field of view, radians, 0 < fov_y < pi */
+  double near_plane;        /* 0 < near < far */
+  double far_plane;
+  float bg[3];              /* background colour */
+  int d_max;                /* max reuse depth D_max >= 1 (10 in the paper) */
+  unsigned flags;           /* GSC_F_* */
+  int64_t pair_capacity;    /* max (tile, depth) pairs per frame; 0 = default */
+} gsc_config;
+
+typedef struct { double p[3]; double q[4]; } gsc_eye;
+typedef struct { gsc_eye left, right; double timestamp; } gsc_rig; /* StereoRig */
+
+/* Host-side view of a scene (SoA, little-endian).  Borrowed by
+ * gsc_load_scene_host for the duration of the call only.  Feature and weight
+ * values are int8 codes on the 2^-7 grid (value = code / 128). */
+typedef struct {
+  int32_t n_anchors, lod_levels;  /* N, L */
+  float d0;                       /* LoD base distance */
+  const float *pos;               /* [N][3] */
+  const int8_t *feat;             /* [N][32] */
+  const float *offs;              /* [N][10][3] */
+  const float *scale;             /* [N][3] */
+  const uint8_t *level;           /* [N] */
+  const int8_t *W1;               /* [35][96] (alpha | colour | covariance heads) */
+  const int8_t *b1;               /* [96] */
+  const int8_t *W2a, *b2a;        /* [32][10], [10] */
+  const int8_t *W2c, *b2c;        /* [32][30], [30] */
+  const int8_t *W2s, *b2s;        /* [32][70], [70]: per Gaussian 3 scales then quaternion (w,x,y,z) */
+} gsc_scene_desc;
+
+/* Per-frame record (SPEC FrameRecord S:421-423, CacheStats S:208). */
+typedef struct {
+  int64_t frame;
+  uint32_t n_visible, n_hits, n_misses, n_new;   /* |X_f|, hits, misses (decoded), |X_f \ X_f-1| */
+  uint32_t n_splats;                             /* projected splats with >= 1 tile, both eyes */
+  uint32_t overflow;                             /* 1 if pairs exceeded pair_capacity */
+  uint64_t n_pairs;                              /* (tile, depth) pairs, both eyes */
+  int32_t depth_used, depth_next;                /* reuse depth for this frame / the next */
+  float update_rate, novelty_rate;               /* misses/|X_f|, new/|X_f| */
+  /* stage times in ms (GSC_F_STAGE_TIMING; else 0): */
+  float ms_cull, ms_derive, ms_project, ms_depth_sort, ms_emit, ms_tile_sort, ms_ranges, ms_blend, ms_total;
+} gsc_frame_stats;
+
+/* out formats */
+#define GSC_FMT_RGB_F32_PLANAR 0
+#define GSC_FMT_RGBA8 1
+
+/* debug fetch selectors (gsc_debug_fetch; call after the frame's stream work finished) */
+#define GSC_DBG_VISIBLE 1     /* uint32 anchor ids of X_f, ascending */
+#define GSC_DBG_MISSES 2      /* uint32 anchor ids decoded this frame, ascending */
+#define GSC_DBG_POOL 3        /* float [N*10][13]: alpha, mu[3], cov[6] (00 01 02 11 12 22), rgb[3] by slot g=i*10+j */
+#define GSC_DBG_SPLATS 4      /* float [n_splats][12]: u v A B C alpha r g b depth thr eye ; ordered by (eye, slot) */
+#define GSC_DBG_SPLAT_G 5     /* uint32 [n_splats]: Gaussian slot g of each splat (same order) */
+#define GSC_DBG_PAIRS 6       /* uint64 [n_pairs]: sorted (tile << 32 | depth bits), tile = eye*T_e + ty*TW + tx */
+#define GSC_DBG_PAIR_G 7      /* uint32 [n_pairs]: Gaussian slot g of each sorted pair */
+#define GSC_DBG_RANGES 8      /* uint32 [2*T_e][2]: [start, end) per (eye, tile) */
+#define GSC_DBG_BIRTH 9       /* int32 [N]: frame each anchor's pool slots were derived (INT32_MIN: never) */
+
+int gsc_abi_version(void);
+
+/* Create a context on CUDA device `cuda_device`.  Validates cfg (GSC_EINVAL). */
+gsc_status gsc_create(int cuda_device, const gsc_config *cfg, gsc_ctx **out);
+
+/* Load a GSC2 scene file (format in scenegen/__init__.py write_gsc2); resets the cache.
+ * GSC_EFORMAT with the byte offset on bad magic / truncation / unsupported dims. */
+gsc_status gsc_load_scene(gsc_ctx *ctx, const char *path);
+
+/* Same from host arrays (copied to the device; the caller keeps ownership). */
+gsc_status gsc_load_scene_host(gsc_ctx *ctx, const gsc_scene_desc *scene);
+
+/* Validate the rig (unit quaternions within 1e-6) and compute the
+ * unified camera (Eqs. 5-6) and per-eye constants for the next render.
+ * GSC_EDEGENERATE for antiparallel eyes. */
+gsc_status gsc_set_pose(gsc_ctx *ctx, const gsc_rig *rig);
+
+/* Enqueue one binocular frame on `cuda_stream` (NULL: the legacy default
+ * stream) writing caller-owned DEVICE buffers out_left / out_right in
+ * `out_format`.  Returns after enqueueing; results and stats are valid after
+ * the stream synchronises.  If `stats` is non-NULL the call synchronises the
+ * stream before returning and fills it. */
+gsc_status gsc_render_pair(gsc_ctx *ctx, void *out_left, void *out_right, int out_format,
+                           void *cuda_stream, gsc_frame_stats *stats);
+
+/* End-to-end call: set the pose from HOST memory, render, copy both images
+ * into caller-owned HOST buffers (pinned for full speed), synchronise.
+ * `stats` may be NULL. */
+gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
+                                int out_format, gsc_frame_stats *stats);
+
+/* Wait for the context's outstanding work on `cuda_stream`. */
+gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream);
+
+/* Per-frame records of the last `max` frames rendered since the previous call
+ * (oldest first).  Call after gsc_sync.  *n receives the count. */
+gsc_status gsc_stats_history(gsc_ctx *ctx, gsc_frame_stats *dst, int max, int *n);
+
+/* Drop every cache line and restart the frame counter at 0 (Alg. 1 "first frame"). */
+gsc_status gsc_reset_cache(gsc_ctx *ctx);
+
+/* Copy an intermediate of the most recent frame to host memory (debug/parity).
+ * *len_bytes receives the full size; at most capacity_bytes are written.
+ * Synchronises the context's last stream. */
+gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t capacity_bytes, size_t *len_bytes);
+
+/* Evaluate the device elementary functions (0 exp_s, 1 log_s, 2 tanh_s,
+ * 3 sigmoid_s; DESIGN.md Numerics) on n device floats (parity sweeps). */
+gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n);
+
+const char *gsc_last_error(const gsc_ctx *ctx);
+void gsc_destroy(gsc_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GSCACHE_H */

@@ -1,0 +1,108 @@
+// blend.cu -- SURVEY §8(a) row a8: per-tile front-to-back alpha compositing
+// for both eyes (Eq. 1; Alg. 1; reading R17).
+//
+// One 256-thread CTA per (eye, 16x16 tile), one pixel per thread; the tile's
+// depth-sorted splats are staged through shared memory in batches of 256
+// (36 bytes each: float4 (u,v,A,B), float4 (C,alpha,r,g), float b); the CTA
+// leaves as soon as every pixel of the tile has terminated
+// (__syncthreads_count).  Per (pixel, splat), in the exact op order of
+// DESIGN.md Numerics N6:
+//   power = -0.5 (A dx^2 + C dy^2) - B dx dy      (skip if > 0)
+//   alpha' = min(0.99, alpha exp_s(power))        (skip if < 1/255)
+//   T' = T (1 - alpha'); stop before T' < 1e-4; C += c (alpha' T); T = T'
+// power < -5.55 is skipped without evaluating exp_s: exp_s(-5.55) < 1/255
+// and alpha <= 1, so the skip decision is identical (N5).
+#include "gsc_internal.cuh"
+
+namespace gsc {
+
+constexpr int kBThreads = 256;
+
+__global__ void __launch_bounds__(kBThreads)
+blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
+             const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
+             void *__restrict__ out_l, void *__restrict__ out_r, int fmt) {
+  __shared__ float4 sA[kBThreads];
+  __shared__ float4 sB[kBThreads];
+  __shared__ float sb[kBThreads];
+  const int t = threadIdx.x;
+  const int tile = blockIdx.x;
+  const int e = tile >= fc.Te;
+  const int tl = tile - e * fc.Te;
+  const int tx = tl % fc.TW, ty = tl / fc.TW;
+  const int px = tx * kTile + (t & 15), py = ty * kTile + (t >> 4);
+  const bool inside = px < fc.width && py < fc.height;
+  const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
+  const uint2 rg = ranges[tile];
+  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+  int done = !inside;
+  for (uint32_t b = rg.x; b < rg.y; b += kBThreads) {
+    __syncthreads();
+    uint32_t idx = b + t;
+    if (idx < rg.y) {
+      uint32_t c = pair_vals[idx];
+      sA[t] = spA[c];
+      sB[t] = spB[c];
+      sb[t] = spC[c].x;
+    }
+    __syncthreads();
+    const int cnt = min((uint32_t)kBThreads, rg.y - b);
+    if (!done) {
+      for (int k = 0; k < cnt; ++k) {
+        const float4 a = sA[k];
+        const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
+        const float4 q = sB[k];
+        const float power = __fsub_rn(
+            __fmul_rn(-0.5f, __fadd_rn(__fmul_rn(a.z, __fmul_rn(dx, dx)), __fmul_rn(q.x, __fmul_rn(dy, dy)))),
+            __fmul_rn(a.w, __fmul_rn(dx, dy)));
+        if (power > 0.0f || power < -5.55f) continue;
+        const float al = fminf(0.99f, __fmul_rn(q.y, exp_s(power)));
+        if (al < kAlphaMin) continue;
+        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
+        if (Tn < 0.0001f) { done = 1; break; }
+        const float w = __fmul_rn(al, T);
+        C0 = __fadd_rn(C0, __fmul_rn(q.z, w));
+        C1 = __fadd_rn(C1, __fmul_rn(q.w, w));
+        C2 = __fadd_rn(C2, __fmul_rn(sb[k], w));
+        T = Tn;
+      }
+    }
+    if (__syncthreads_count(done) == kBThreads) break;
+  }
+  if (!inside) return;
+  const float o0 = __fadd_rn(C0, __fmul_rn(T, fc.bg[0]));
+  const float o1 = __fadd_rn(C1, __fmul_rn(T, fc.bg[1]));
+  const float o2 = __fadd_rn(C2, __fmul_rn(T, fc.bg[2]));
+  void *out = e ? out_r : out_l;
+  const size_t HW = (size_t)fc.width * fc.height, pix = (size_t)py * fc.width + px;
+  if (fmt == 0) {
+    float *o = reinterpret_cast<float *>(out);
+    o[pix] = o0;
+    o[HW + pix] = o1;
+    o[2 * HW + pix] = o2;
+  } else {
+    auto q8 = [](float x) -> uint32_t {
+      float y = fminf(fmaxf(__fmul_rn(x, 255.0f), 0.0f), 255.0f);
+      return (uint32_t)__float2int_rn(y);
+    };
+    reinterpret_cast<uint32_t *>(out)[pix] = q8(o0) | (q8(o1) << 8) | (q8(o2) << 16) | (q8(1.0f - T) << 24);
+  }
+}
+
+void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_vals, const float4 *spA,
+                  const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, cudaStream_t st) {
+  blend_kernel<<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt);
+}
+
+// elementary-function self test (parity sweeps through the C ABI)
+__global__ void elem_kernel(int fn, const float *__restrict__ in, float *__restrict__ out, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    float x = in[i];
+    out[i] = fn == 0 ? exp_s(x) : fn == 1 ? log_s(x) : fn == 2 ? tanh_s(x) : sigmoid_s(x);
+  }
+}
+void launch_elem(int fn, const float *in, float *out, size_t n, int num_sms, cudaStream_t st) {
+  elem_kernel<<<num_sms * 8, 256, 0, st>>>(fn, in, out, n);
+}
+
+}  // namespace gsc

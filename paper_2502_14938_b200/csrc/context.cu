@@ -1,0 +1,697 @@
+// context.cu -- host runtime and the C ABI of include/gscache.h.
+//
+// Owns the device-resident scene (SoA), the persistent Gaussian pool (the
+// cache), the cache-policy state, all per-frame buffers, and drives
+// the per-frame kernel sequence of SURVEY §3 (3) on the caller's stream.
+// No host synchronisation inside a frame: every data-dependent size (V, M,
+// splats, pairs) stays on the device and the kernels read it there.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/gscache.h"
+#include "gsc_internal.cuh"
+
+namespace gsc {
+// launchers (kernels in the other translation units)
+void launch_cull(const FrameC &, int, const float4 *, const uint8_t *, int32_t *, const uint32_t *, uint32_t *,
+                 uint32_t *, uint32_t *, unsigned long long *, FrameCounters *, const PolicyState *, cudaStream_t);
+void launch_policy(PolicyState *, const FrameCounters *, FrameRecordDev *, cudaStream_t);
+void launch_record(const FrameCounters *, FrameRecordDev *, cudaStream_t);
+void launch_margin(int, const float *, const float *, const float *, float4 *, cudaStream_t);
+int cull_tiles(int N);
+void launch_derive(const float pu[3], const uint32_t *, const float4 *, const int8_t *, const float *, const float *,
+                   const int8_t *, const int32_t *, const int8_t *, const int32_t *, float *, float4 *,
+                   FrameCounters *, int, cudaStream_t);
+void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, const SplatBufs &, uint32_t *,
+                    FrameCounters *, int, cudaStream_t);
+int project_tile_size();
+void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, const uint32_t *,
+                     uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
+void launch_emit(const EmitIn &, int, int, int, int, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *,
+                 int, cudaStream_t);
+void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
+void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const float4 *, const float4 *, const float4 *,
+                  void *, void *, int, cudaStream_t);
+void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
+int sort_tile_size();
+int emit_tile_size();
+}  // namespace gsc
+
+using namespace gsc;
+
+namespace {
+
+constexpr int kRing = 2048;     // per-frame record / event ring
+constexpr int kEvents = 10;     // stage boundaries per frame
+
+template <typename T>
+struct DevBuf {
+  T *p = nullptr;
+  size_t n = 0;
+  ~DevBuf() { if (p) cudaFree(p); }
+  cudaError_t alloc(size_t count) {
+    if (p) { cudaFree(p); p = nullptr; }
+    n = count;
+    return count ? cudaMalloc(&p, count * sizeof(T)) : cudaSuccess;
+  }
+};
+
+struct FrameSlot {
+  cudaEvent_t ev[kEvents];
+  bool timed = false;
+  bool used = false;
+};
+
+}  // namespace
+
+struct gsc_ctx {
+  int device = 0;
+  gsc_config cfg{};
+  int num_sms = 148;
+  std::string err;
+  bool sticky = false;
+  // scene
+  int N = 0, L = 0;
+  float d0 = 0.0f;
+  bool have_scene = false, have_pose = false;
+  DevBuf<float4> pos_m;
+  DevBuf<uint8_t> level;
+  DevBuf<int8_t> feat;
+  DevBuf<float> offs, scale;
+  DevBuf<int8_t> W1T, W2T;
+  DevBuf<int32_t> b1s, b2s;
+  // cache
+  DevBuf<int32_t> birth;
+  DevBuf<uint32_t> vis[2];
+  int vis_cur = 0;
+  DevBuf<float> alpha;
+  DevBuf<float4> pool;
+  DevBuf<PolicyState> policy;
+  // per frame
+  DevBuf<uint32_t> visible, misses;
+  size_t cap_splat = 0, cap_pairs = 0;
+  DevBuf<float4> spA, spB, spC;
+  DevBuf<uint2> box;
+  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot;
+  DevBuf<uint32_t> pkey_a, pval_a, pkey_b, pval_b;
+  DevBuf<uint2> ranges;
+  DevBuf<uint32_t> sort_status_a, sort_status_b;
+  DevBuf<unsigned char> zero_region;     // FrameCounters | cull status | project status | emit status
+  size_t zero_bytes = 0, off_cull = 0, off_proj = 0, off_emit = 0;
+  DevBuf<FrameRecordDev> rec_dev;
+  FrameRecordDev *rec_host = nullptr;    // pinned ring
+  FrameSlot slots[kRing];
+  int64_t frames_rendered = 0, frames_reported = 0;
+  FrameC fc{};
+  float pu[3] = {0, 0, 0};
+  cudaStream_t last_stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  // e2e staging
+  DevBuf<unsigned char> img_dev[2];
+
+  FrameCounters *ctr() { return reinterpret_cast<FrameCounters *>(zero_region.p); }
+};
+
+static gsc_status fail(gsc_ctx *c, gsc_status s, const std::string &msg) {
+  if (c) {
+    c->err = msg;
+    if (s == GSC_ECUDA) c->sticky = true;
+  }
+  return s;
+}
+#define CU(call)                                                                                   \
+  do {                                                                                             \
+    cudaError_t _e = (call);                                                                       \
+    if (_e != cudaSuccess) return fail(ctx, GSC_ECUDA, std::string(#call ": ") + cudaGetErrorString(_e)); \
+  } while (0)
+
+static bool cfg_valid(const gsc_config *c) {
+  return c && c->width > 0 && c->height > 0 && c->width <= 16 * 65535 && c->fov_y > 0 && c->fov_y < M_PI &&
+         c->near_plane > 0 && c->far_plane > c->near_plane && c->d_max >= 1 &&
+         2LL * ((c->width + 15) / 16) * ((c->height + 15) / 16) <= 65536;
+}
+
+// ----------------------------------------------------------------------------------- camera (a0)
+// Eqs. 5-6 in fp64, rounded once to fp32.  R(q) world-from-camera
+// (S:41), right = R[:,0], up = R[:,1], forward = -R[:,2].
+static bool quat_R(const double qi[4], double R[3][3]) {
+  double n = std::sqrt(qi[0] * qi[0] + qi[1] * qi[1] + qi[2] * qi[2] + qi[3] * qi[3]);
+  if (!(std::fabs(n - 1.0) <= 1e-6)) return false;
+  double w = qi[0] / n, x = qi[1] / n, y = qi[2] / n, z = qi[3] / n;
+  R[0][0] = 1.0 - 2.0 * (y * y + z * z); R[0][1] = 2.0 * (x * y - w * z); R[0][2] = 2.0 * (x * z + w * y);
+  R[1][0] = 2.0 * (x * y + w * z); R[1][1] = 1.0 - 2.0 * (x * x + z * z); R[1][2] = 2.0 * (y * z - w * x);
+  R[2][0] = 2.0 * (x * z - w * y); R[2][1] = 2.0 * (y * z + w * x); R[2][2] = 1.0 - 2.0 * (x * x + y * y);
+  return true;
+}
+
+static gsc_status compute_frame_consts(gsc_ctx *ctx, const gsc_rig *rig) {
+  const gsc_config &c = ctx->cfg;
+  double RL[3][3], RR[3][3];
+  if (!quat_R(rig->left.q, RL) || !quat_R(rig->right.q, RR))
+    return fail(ctx, GSC_EINVAL, "rig quaternion not unit within 1e-6 (S:43)");
+  for (int k = 0; k < 3; ++k)
+    if (!std::isfinite(rig->left.p[k]) || !std::isfinite(rig->right.p[k])) return fail(ctx, GSC_EINVAL, "non-finite eye position");
+  const double ty = std::tan(c.fov_y / 2.0);
+  const double tx = ty * (double)c.width / (double)c.height;
+  const double fy = ((double)c.height / 2.0) / ty;
+  FrameC &fc = ctx->fc;
+  const double (*Rs[2])[3] = {RL, RR};
+  const gsc_eye *eyes[2] = {&rig->left, &rig->right};
+  for (int e = 0; e < 2; ++e) {
+    EyeC &ec = fc.eye[e];
+    for (int k = 0; k < 3; ++k) {
+      ec.p[k] = (float)eyes[e]->p[k];
+      ec.r0[k] = (float)Rs[e][k][0];
+      ec.r1[k] = (float)(-Rs[e][k][1]);
+      ec.r2[k] = (float)(-Rs[e][k][2]);
+    }
+    ec.fx = (float)fy; ec.fy = (float)fy;
+    ec.cx = (float)((double)c.width / 2.0); ec.cy = (float)((double)c.height / 2.0);
+    ec.near_plane = (float)c.near_plane; ec.far_plane = (float)c.far_plane;
+    ec.limx = (float)(1.3 * tx); ec.limy = (float)(1.3 * ty);
+  }
+  double ds[3], us[3], d[3], up[3], rt[3], pm[3], dp[3];
+  for (int k = 0; k < 3; ++k) {
+    ds[k] = (-RL[k][2]) + (-RR[k][2]);
+    us[k] = RL[k][1] + RR[k][1];
+    pm[k] = (rig->left.p[k] + rig->right.p[k]) / 2.0;
+    dp[k] = rig->left.p[k] - rig->right.p[k];
+  }
+  double dn = std::sqrt(ds[0] * ds[0] + ds[1] * ds[1] + ds[2] * ds[2]);
+  if (!(dn > 1e-6)) return fail(ctx, GSC_EDEGENERATE, "antiparallel eye directions (S:296)");
+  for (int k = 0; k < 3; ++k) d[k] = ds[k] / dn;
+  double b = std::sqrt(dp[0] * dp[0] + dp[1] * dp[1] + dp[2] * dp[2]);
+  double pb = b / (2.0 * ty);
+  double ud = us[0] * d[0] + us[1] * d[1] + us[2] * d[2];
+  for (int k = 0; k < 3; ++k) up[k] = us[k] - ud * d[k];
+  double un = std::sqrt(up[0] * up[0] + up[1] * up[1] + up[2] * up[2]);
+  if (!(un > 1e-9)) return fail(ctx, GSC_EDEGENERATE, "eye up vectors degenerate (S:297)");
+  for (int k = 0; k < 3; ++k) up[k] = up[k] / un;
+  rt[0] = d[1] * up[2] - d[2] * up[1];
+  rt[1] = d[2] * up[0] - d[0] * up[2];
+  rt[2] = d[0] * up[1] - d[1] * up[0];
+  UniC &u = fc.u;
+  for (int k = 0; k < 3; ++k) {
+    u.p[k] = (float)(pm[k] - d[k] * pb);
+    u.fwd[k] = (float)d[k];
+    u.up[k] = (float)up[k];
+    u.right[k] = (float)rt[k];
+    ctx->pu[k] = u.p[k];
+  }
+  u.near_plane = (float)c.near_plane;
+  u.far_plane = (float)(c.far_plane + pb);
+  u.tx = (float)tx; u.ty = (float)ty;
+  u.kx = (float)std::sqrt(1.0 + tx * tx); u.ky = (float)std::sqrt(1.0 + ty * ty);
+  fc.width = c.width; fc.height = c.height;
+  fc.TW = (c.width + kTile - 1) / kTile;
+  fc.TH = (c.height + kTile - 1) / kTile;
+  fc.Te = fc.TW * fc.TH;
+  fc.L = ctx->L; fc.d0 = ctx->d0;
+  for (int k = 0; k < 3; ++k) fc.bg[k] = c.bg[k];
+  return GSC_OK;
+}
+
+// ----------------------------------------------------------------------------------- scene load
+static gsc_status reset_cache(gsc_ctx *ctx, cudaStream_t st);
+
+static __global__ void fill_i32(int32_t *p, size_t n, int32_t v) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
+  const int N = s->n_anchors;
+  if (N <= 0 || s->lod_levels < 1 || s->lod_levels > 64 || !(s->d0 > 0.0f) || !s->pos || !s->feat || !s->offs ||
+      !s->scale || !s->level || !s->W1 || !s->b1 || !s->W2a || !s->b2a || !s->W2c || !s->b2c || !s->W2s || !s->b2s)
+    return fail(ctx, GSC_EINVAL, "invalid scene description");
+  if ((int64_t)N * kK >= (1LL << 29)) return fail(ctx, GSC_EINVAL, "scene too large (N*K must be < 2^29)");
+  for (int i = 0; i < N; ++i)
+    if (s->level[i] >= s->lod_levels) return fail(ctx, GSC_EFORMAT, "anchor level >= L at anchor " + std::to_string(i));
+  // exact int32 range of the grid MLP (R3): |z1| <= hmax, |z2| < 2^31
+  int64_t hmax = 0;
+  for (int n = 0; n < 96; ++n) {
+    int64_t acc = 128 * (int64_t)std::abs((int)s->b1[n]);
+    for (int k = 0; k < kF + 3; ++k) acc += 127 * (int64_t)std::abs((int)s->W1[k * 96 + n]);
+    hmax = std::max(hmax, acc);
+  }
+  std::vector<int8_t> W1T(96 * 36, 0), W2T(kNOut * 32, 0);
+  std::vector<int32_t> b1s(96), b2s(kNOut);
+  for (int n = 0; n < 96; ++n) {
+    for (int k = 0; k < kF + 3; ++k) W1T[n * 36 + k] = s->W1[k * 96 + n];
+    b1s[n] = 128 * (int32_t)s->b1[n];
+  }
+  for (int m = 0; m < kNOut; ++m) {
+    const int8_t *W2; int nh, mm; int8_t b;
+    if (m < kK) { W2 = s->W2a; nh = kK; mm = m; b = s->b2a[mm]; }
+    else if (m < 4 * kK) { W2 = s->W2c; nh = 3 * kK; mm = m - kK; b = s->b2c[mm]; }
+    else { W2 = s->W2s; nh = 7 * kK; mm = m - 4 * kK; b = s->b2s[mm]; }
+    int64_t bound = 16384 * (int64_t)std::abs((int)b);
+    for (int u = 0; u < 32; ++u) {
+      W2T[m * 32 + u] = W2[u * nh + mm];
+      bound += hmax * std::abs((int)W2[u * nh + mm]);
+    }
+    if (bound >= (1LL << 31)) return fail(ctx, GSC_EFORMAT, "decoder weights exceed the exact int32 range");
+    b2s[m] = 16384 * (int32_t)b;
+  }
+  ctx->have_scene = false;
+  ctx->N = N; ctx->L = s->lod_levels; ctx->d0 = s->d0;
+  const size_t NK = (size_t)N * kK;
+  CU(ctx->pos_m.alloc(N));
+  CU(ctx->level.alloc(N));
+  CU(ctx->feat.alloc((size_t)N * kF));
+  CU(ctx->offs.alloc(NK * 3));
+  CU(ctx->scale.alloc((size_t)N * 3));
+  CU(ctx->W1T.alloc(96 * 36));
+  CU(ctx->W2T.alloc(kNOut * 32));
+  CU(ctx->b1s.alloc(96));
+  CU(ctx->b2s.alloc(kNOut));
+  DevBuf<float> pos;
+  CU(pos.alloc((size_t)N * 3));
+  CU(cudaMemcpy(pos.p, s->pos, (size_t)N * 12, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->level.p, s->level, N, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->feat.p, s->feat, (size_t)N * kF, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->offs.p, s->offs, NK * 12, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->scale.p, s->scale, (size_t)N * 12, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->W1T.p, W1T.data(), W1T.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->W2T.p, W2T.data(), W2T.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->b1s.p, b1s.data(), 96 * 4, cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(ctx->b2s.p, b2s.data(), kNOut * 4, cudaMemcpyHostToDevice));
+  launch_margin(N, pos.p, ctx->offs.p, ctx->scale.p, ctx->pos_m.p, nullptr);
+  CU(cudaGetLastError());
+  // cache + per-frame buffers
+  CU(ctx->birth.alloc(N));
+  const size_t words = ((size_t)N + 31) / 32 + 1;
+  CU(ctx->vis[0].alloc(words));
+  CU(ctx->vis[1].alloc(words));
+  CU(ctx->alpha.alloc(NK));
+  CU(ctx->pool.alloc(NK * 3));
+  CU(cudaMemset(ctx->alpha.p, 0, NK * 4));
+  CU(cudaMemset(ctx->pool.p, 0, NK * 48));
+  CU(ctx->visible.alloc(N));
+  CU(ctx->misses.alloc(N));
+  ctx->cap_splat = 2 * NK;
+  CU(ctx->spA.alloc(ctx->cap_splat));
+  CU(ctx->spB.alloc(ctx->cap_splat));
+  CU(ctx->spC.alloc(ctx->cap_splat));
+  CU(ctx->box.alloc(ctx->cap_splat));
+  CU(ctx->count.alloc(ctx->cap_splat));
+  CU(ctx->gslot.alloc(ctx->cap_splat));
+  CU(ctx->dkey_a.alloc(ctx->cap_splat));
+  CU(ctx->dval_a.alloc(ctx->cap_splat));
+  CU(ctx->dkey_b.alloc(ctx->cap_splat));
+  CU(ctx->dval_b.alloc(ctx->cap_splat));
+  int64_t pc = ctx->cfg.pair_capacity > 0 ? ctx->cfg.pair_capacity : std::max<int64_t>(1 << 24, 4 * (int64_t)NK);
+  pc = std::min<int64_t>(pc, (1LL << 30) - 1);
+  ctx->cap_pairs = (size_t)pc;
+  CU(ctx->pkey_a.alloc(ctx->cap_pairs));
+  CU(ctx->pval_a.alloc(ctx->cap_pairs));
+  CU(ctx->pkey_b.alloc(ctx->cap_pairs));
+  CU(ctx->pval_b.alloc(ctx->cap_pairs));
+  const int TW = (ctx->cfg.width + 15) / 16, TH = (ctx->cfg.height + 15) / 16;
+  CU(ctx->ranges.alloc(2 * (size_t)TW * TH));
+  const size_t stiles = (std::max(ctx->cap_splat, ctx->cap_pairs) + sort_tile_size() - 1) / sort_tile_size();
+  CU(ctx->sort_status_a.alloc(stiles * 256));
+  CU(ctx->sort_status_b.alloc(stiles * 256));
+  CU(cudaMemset(ctx->sort_status_a.p, 0, stiles * 1024));
+  CU(cudaMemset(ctx->sort_status_b.p, 0, stiles * 1024));
+  auto al = [](size_t x) { return (x + 255) & ~size_t(255); };
+  ctx->off_cull = al(sizeof(FrameCounters));
+  ctx->off_proj = ctx->off_cull + al((size_t)cull_tiles(N) * 8);
+  ctx->off_emit = ctx->off_proj + al((ctx->cap_splat / 2 + project_tile_size() - 1) / project_tile_size() * 4);
+  ctx->zero_bytes = ctx->off_emit + al((ctx->cap_splat + emit_tile_size() - 1) / emit_tile_size() * 4);
+  CU(ctx->zero_region.alloc(ctx->zero_bytes));
+  CU(cudaMemset(ctx->zero_region.p, 0, ctx->zero_bytes));
+  CU(cudaDeviceSynchronize());
+  ctx->have_scene = true;
+  return reset_cache(ctx, nullptr);
+}
+
+static gsc_status reset_cache(gsc_ctx *ctx, cudaStream_t st) {
+  if (!ctx->have_scene) return fail(ctx, GSC_ESTATE, "no scene loaded");
+  fill_i32<<<ctx->num_sms * 4, 256, 0, st>>>(ctx->birth.p, ctx->N, INT32_MIN);
+  CU(cudaGetLastError());
+  CU(cudaMemsetAsync(ctx->vis[0].p, 0, ctx->vis[0].n * 4, st));
+  CU(cudaMemsetAsync(ctx->vis[1].p, 0, ctx->vis[1].n * 4, st));
+  PolicyState ps{};
+  ps.frame = 0;
+  ps.depth = ctx->cfg.d_max;              // Alg. 1 l.182 / frame 0 keeps D_max
+  ps.W = -ctx->cfg.d_max;                 // W_0 = 0 - depth_0
+  ps.d_max = ctx->cfg.d_max;
+  ps.literal = (ctx->cfg.flags & GSC_F_DEPTH_LITERAL) ? 1 : 0;
+  CU(cudaMemcpyAsync(ctx->policy.p, &ps, sizeof(ps), cudaMemcpyHostToDevice, st));
+  CU(cudaStreamSynchronize(st));
+  return GSC_OK;
+}
+
+// ----------------------------------------------------------------------------------- GSC2 file
+static gsc_status load_file(gsc_ctx *ctx, const char *path) {
+  std::ifstream f(path, std::ios::binary);
+  if (!f) return fail(ctx, GSC_EINVAL, std::string("cannot open ") + path);
+  std::vector<char> buf((std::istreambuf_iterator<char>(f)), std::istreambuf_iterator<char>());
+  const size_t hdr = 4 + 6 * 4 + 4 + 24;
+  if (buf.size() < hdr) return fail(ctx, GSC_EFORMAT, "truncated header at offset " + std::to_string(buf.size()));
+  if (std::memcmp(buf.data(), "GSC2", 4) != 0) return fail(ctx, GSC_EFORMAT, "bad magic at offset 0");
+  uint32_t u[6];
+  std::memcpy(u, buf.data() + 4, 24);
+  if (u[0] != 2) return fail(ctx, GSC_EFORMAT, "unsupported version at offset 4");
+  const uint32_t N = u[1], F = u[2], K = u[3], L = u[4], H = u[5];
+  if (F != (uint32_t)kF || K != (uint32_t)kK || H != (uint32_t)kH)
+    return fail(ctx, GSC_EFORMAT, "unsupported F/K/H at offset 12 (need 32/10/32)");
+  float d0;
+  std::memcpy(&d0, buf.data() + 28, 4);
+  size_t off = hdr;
+  auto take = [&](size_t bytes, const char *what, const void **ptr) -> bool {
+    if (off + bytes > buf.size()) return false;
+    *ptr = buf.data() + off;
+    off += bytes;
+    return true;
+  };
+  gsc_scene_desc s{};
+  s.n_anchors = (int32_t)N; s.lod_levels = (int32_t)L; s.d0 = d0;
+  const void *p;
+  struct { size_t bytes; const void **dst; } items[] = {
+      {N * 12ull, (const void **)&s.pos}, {N * 32ull, (const void **)&s.feat}, {N * 120ull, (const void **)&s.offs},
+      {N * 12ull, (const void **)&s.scale}, {N * 1ull, (const void **)&s.level}, {35 * 96ull, (const void **)&s.W1},
+      {96ull, (const void **)&s.b1}, {32 * 10ull, (const void **)&s.W2a}, {10ull, (const void **)&s.b2a},
+      {32 * 30ull, (const void **)&s.W2c}, {30ull, (const void **)&s.b2c}, {32 * 70ull, (const void **)&s.W2s},
+      {70ull, (const void **)&s.b2s}};
+  for (auto &it : items) {
+    if (!take(it.bytes, "", &p)) return fail(ctx, GSC_EFORMAT, "truncated at offset " + std::to_string(off));
+    *it.dst = p;
+  }
+  return upload_scene(ctx, &s);
+}
+
+// ----------------------------------------------------------------------------------- frame
+static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaStream_t st) {
+  if (ctx->sticky) return fail(ctx, GSC_ECUDA, "context has a sticky CUDA error: " + ctx->err);
+  if (!ctx->have_scene || !ctx->have_pose) return fail(ctx, GSC_ESTATE, "render before load_scene/set_pose");
+  if (!out_l || !out_r || (fmt != GSC_FMT_RGB_F32_PLANAR && fmt != GSC_FMT_RGBA8))
+    return fail(ctx, GSC_EINVAL, "bad output buffers or format");
+  ctx->last_stream = st;
+  const int slot_i = (int)(ctx->frames_rendered % kRing);
+  FrameSlot &slot = ctx->slots[slot_i];
+  const bool timed = (ctx->cfg.flags & GSC_F_STAGE_TIMING) != 0;
+  if (timed && !slot.timed) {
+    for (int k = 0; k < kEvents; ++k) CU(cudaEventCreate(&slot.ev[k]));
+    slot.timed = true;
+  }
+  int evk = 0;
+  auto mark = [&]() { if (timed) cudaEventRecord(slot.ev[evk++], st); };
+  FrameCounters *ctr = ctx->ctr();
+  const FrameC &fc = ctx->fc;
+  mark();
+  CU(cudaMemsetAsync(ctx->zero_region.p, 0, ctx->zero_bytes, st));
+  CU(cudaMemsetAsync(ctx->ranges.p, 0, ctx->ranges.n * sizeof(uint2), st));
+  const int cur = ctx->vis_cur;
+  // a1 + a2
+  launch_cull(fc, ctx->N, ctx->pos_m.p, ctx->level.p, ctx->birth.p, ctx->vis[cur ^ 1].p, ctx->vis[cur].p,
+              ctx->visible.p, ctx->misses.p, reinterpret_cast<unsigned long long *>(ctx->zero_region.p + ctx->off_cull),
+              ctr, ctx->policy.p, st);
+  launch_policy(ctx->policy.p, ctr, ctx->rec_dev.p + slot_i, st);
+  mark();
+  // a3
+  launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p, ctx->b1s.p,
+                ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, st);
+  mark();
+  // a4
+  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p};
+  launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, sb,
+                 reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
+  mark();
+  // a5 (depth digits of the (tile, depth) sort)
+  launch_onesweep(ctx->dkey_a.p, ctx->dval_a.p, ctx->dkey_b.p, ctx->dval_b.p, true, &ctr->n_splat, 4,
+                  &ctr->hist_depth[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[0],
+                  ctx->num_sms, st);
+  mark();
+  EmitIn ei{ctx->dval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p};
+  launch_emit(ei, fc.width, fc.height, fc.TW, fc.Te, (uint32_t)ctx->cap_pairs, ctx->pkey_a.p, ctx->pval_a.p,
+              reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_emit), ctr, ctx->num_sms, st);
+  mark();
+  // a6 (tile digits)
+  launch_onesweep(ctx->pkey_a.p, ctx->pval_a.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2,
+                  &ctr->hist_tile[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[4],
+                  ctx->num_sms, st);
+  mark();
+  // a7
+  launch_ranges(ctx->pkey_a.p, ctr, ctx->ranges.p, ctx->num_sms, st);
+  mark();
+  // a8
+  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, st);
+  launch_record(ctr, ctx->rec_dev.p + slot_i, st);
+  CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
+                     st));
+  mark();
+  CU(cudaGetLastError());
+  slot.used = true;
+  ctx->vis_cur ^= 1;
+  ++ctx->frames_rendered;
+  return GSC_OK;
+}
+
+static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
+  const int slot_i = (int)(frame_seq % kRing);
+  const FrameRecordDev &r = ctx->rec_host[slot_i];
+  std::memset(s, 0, sizeof(*s));
+  s->frame = r.frame;
+  s->n_visible = r.n_visible;
+  s->n_misses = r.n_miss;
+  s->n_hits = r.n_visible - r.n_miss;
+  s->n_new = r.n_new;
+  s->n_splats = r.n_splat;
+  s->n_pairs = r.n_pairs_raw;
+  s->overflow = r.overflow;
+  s->depth_used = r.depth_used;
+  s->depth_next = r.depth_next;
+  s->update_rate = r.n_visible ? (float)r.n_miss / (float)r.n_visible : 0.0f;
+  s->novelty_rate = r.n_visible ? (float)r.n_new / (float)r.n_visible : 0.0f;
+  FrameSlot &slot = ctx->slots[slot_i];
+  if (slot.timed && (ctx->cfg.flags & GSC_F_STAGE_TIMING)) {
+    float ms[kEvents - 1] = {0};
+    for (int k = 0; k + 1 < kEvents; ++k) cudaEventElapsedTime(&ms[k], slot.ev[k], slot.ev[k + 1]);
+    s->ms_cull = ms[0]; s->ms_derive = ms[1]; s->ms_project = ms[2]; s->ms_depth_sort = ms[3];
+    s->ms_emit = ms[4]; s->ms_tile_sort = ms[5]; s->ms_ranges = ms[6]; s->ms_blend = ms[7];
+    cudaEventElapsedTime(&s->ms_total, slot.ev[0], slot.ev[8]);
+  }
+}
+
+// ----------------------------------------------------------------------------------- C ABI
+extern "C" {
+
+int gsc_abi_version(void) { return GSC_ABI_VERSION; }
+
+gsc_status gsc_create(int cuda_device, const gsc_config *cfg, gsc_ctx **out) {
+  if (!out) return GSC_EINVAL;
+  *out = nullptr;
+  if (!cfg_valid(cfg)) return GSC_EINVAL;
+  std::unique_ptr<gsc_ctx> c(new gsc_ctx());
+  gsc_ctx *ctx = c.get();
+  ctx->device = cuda_device;
+  ctx->cfg = *cfg;
+  CU(cudaSetDevice(cuda_device));
+  CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device));
+  CU(ctx->policy.alloc(1));
+  CU(ctx->rec_dev.alloc(kRing));
+  CU(cudaMallocHost(&ctx->rec_host, kRing * sizeof(FrameRecordDev)));
+  std::memset(ctx->rec_host, 0, kRing * sizeof(FrameRecordDev));
+  *out = c.release();
+  return GSC_OK;
+}
+
+gsc_status gsc_load_scene(gsc_ctx *ctx, const char *path) {
+  if (!ctx || !path) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  return load_file(ctx, path);
+}
+
+gsc_status gsc_load_scene_host(gsc_ctx *ctx, const gsc_scene_desc *scene) {
+  if (!ctx || !scene) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  return upload_scene(ctx, scene);
+}
+
+gsc_status gsc_set_pose(gsc_ctx *ctx, const gsc_rig *rig) {
+  if (!ctx || !rig) return GSC_EINVAL;
+  gsc_status s = compute_frame_consts(ctx, rig);
+  if (s == GSC_OK) ctx->have_pose = true;
+  return s;
+}
+
+gsc_status gsc_render_pair(gsc_ctx *ctx, void *out_left, void *out_right, int out_format, void *cuda_stream,
+                           gsc_frame_stats *stats) {
+  if (!ctx) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  gsc_status s = render(ctx, out_left, out_right, out_format, st);
+  if (s != GSC_OK) return s;
+  if (stats) {
+    CU(cudaStreamSynchronize(st));
+    fill_stats(ctx, ctx->frames_rendered - 1, stats);
+    ctx->frames_reported = ctx->frames_rendered;
+    if (stats->overflow) return fail(ctx, GSC_ECAPACITY, "pair capacity exceeded: needed " + std::to_string(stats->n_pairs));
+  }
+  return GSC_OK;
+}
+
+gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right, int out_format,
+                                gsc_frame_stats *stats) {
+  if (!ctx || !rig || !host_left || !host_right) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  gsc_status s = gsc_set_pose(ctx, rig);
+  if (s != GSC_OK) return s;
+  if (!ctx->own_stream) CU(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
+  const size_t bytes = (size_t)ctx->cfg.width * ctx->cfg.height * (out_format == GSC_FMT_RGBA8 ? 4 : 12);
+  for (int e = 0; e < 2; ++e)
+    if (ctx->img_dev[e].n < bytes) CU(ctx->img_dev[e].alloc(bytes));
+  s = render(ctx, ctx->img_dev[0].p, ctx->img_dev[1].p, out_format, ctx->own_stream);
+  if (s != GSC_OK) return s;
+  CU(cudaMemcpyAsync(host_left, ctx->img_dev[0].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
+  CU(cudaMemcpyAsync(host_right, ctx->img_dev[1].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
+  CU(cudaStreamSynchronize(ctx->own_stream));
+  if (stats) {
+    fill_stats(ctx, ctx->frames_rendered - 1, stats);
+    if (stats->overflow) return fail(ctx, GSC_ECAPACITY, "pair capacity exceeded");
+  }
+  return GSC_OK;
+}
+
+gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream) {
+  if (!ctx) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));
+  if (ctx->own_stream) CU(cudaStreamSynchronize(ctx->own_stream));
+  return GSC_OK;
+}
+
+gsc_status gsc_stats_history(gsc_ctx *ctx, gsc_frame_stats *dst, int max, int *n) {
+  if (!ctx || !n || (max > 0 && !dst)) return GSC_EINVAL;
+  int64_t first = std::max(ctx->frames_reported, ctx->frames_rendered - (int64_t)kRing);
+  int64_t cnt = ctx->frames_rendered - first;
+  if (cnt > max) { first = ctx->frames_rendered - max; cnt = max; }
+  for (int64_t k = 0; k < cnt; ++k) fill_stats(ctx, first + k, dst + k);
+  *n = (int)cnt;
+  ctx->frames_reported = ctx->frames_rendered;
+  return GSC_OK;
+}
+
+gsc_status gsc_reset_cache(gsc_ctx *ctx) {
+  if (!ctx) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaDeviceSynchronize());
+  return reset_cache(ctx, nullptr);
+}
+
+gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, size_t *len) {
+  if (!ctx || !len) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaDeviceSynchronize());
+  if (!ctx->have_scene || ctx->frames_rendered == 0) return fail(ctx, GSC_ESTATE, "no frame rendered");
+  FrameCounters c;
+  CU(cudaMemcpy(&c, ctx->zero_region.p, sizeof(c), cudaMemcpyDeviceToHost));
+  const size_t NK = (size_t)ctx->N * kK;
+  const size_t ns = c.n_splat, np = c.n_pairs;
+  auto copy_dev = [&](const void *src, size_t bytes) -> gsc_status {
+    *len = bytes;
+    if (host_dst && cap) CU(cudaMemcpy(host_dst, src, std::min(cap, bytes), cudaMemcpyDeviceToHost));
+    return GSC_OK;
+  };
+  switch (what) {
+    case GSC_DBG_VISIBLE: return copy_dev(ctx->visible.p, (size_t)c.n_visible * 4);
+    case GSC_DBG_MISSES: return copy_dev(ctx->misses.p, (size_t)c.n_miss * 4);
+    case GSC_DBG_BIRTH: return copy_dev(ctx->birth.p, (size_t)ctx->N * 4);
+    case GSC_DBG_SPLAT_G: return copy_dev(ctx->gslot.p, ns * 4);
+    case GSC_DBG_PAIR_G: {
+      *len = np * 4;
+      if (!host_dst || !cap) return GSC_OK;
+      std::vector<uint32_t> pv(np), gs(ns);
+      CU(cudaMemcpy(pv.data(), ctx->pval_a.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(gs.data(), ctx->gslot.p, ns * 4, cudaMemcpyDeviceToHost));
+      std::vector<uint32_t> out(np);
+      for (size_t k = 0; k < np; ++k) out[k] = gs[pv[k]];
+      std::memcpy(host_dst, out.data(), std::min(cap, np * 4));
+      return GSC_OK;
+    }
+    case GSC_DBG_PAIRS: {
+      *len = np * 8;
+      if (!host_dst || !cap) return GSC_OK;
+      std::vector<uint32_t> pk(np), pv(np);
+      std::vector<float4> C(ns);
+      CU(cudaMemcpy(pk.data(), ctx->pkey_a.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(pv.data(), ctx->pval_a.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(C.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
+      std::vector<uint64_t> out(np);
+      for (size_t k = 0; k < np; ++k) {
+        uint32_t db;
+        std::memcpy(&db, &C[pv[k]].z, 4);
+        out[k] = ((uint64_t)pk[k] << 32) | db;
+      }
+      std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
+      return GSC_OK;
+    }
+    case GSC_DBG_RANGES: return copy_dev(ctx->ranges.p, ctx->ranges.n * 8);
+    case GSC_DBG_POOL: {
+      *len = NK * 13 * 4;
+      if (!host_dst || !cap) return GSC_OK;
+      std::vector<float> a(NK);
+      std::vector<float4> p(NK * 3);
+      CU(cudaMemcpy(a.data(), ctx->alpha.p, NK * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(p.data(), ctx->pool.p, NK * 48, cudaMemcpyDeviceToHost));
+      std::vector<float> out(NK * 13);
+      for (size_t g = 0; g < NK; ++g) {
+        const float4 &q0 = p[3 * g], &q1 = p[3 * g + 1], &q2 = p[3 * g + 2];
+        float r[13] = {a[g], q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w};
+        std::memcpy(&out[13 * g], r, sizeof(r));
+      }
+      std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));
+      return GSC_OK;
+    }
+    case GSC_DBG_SPLATS: {
+      *len = ns * 12 * 4;
+      if (!host_dst || !cap) return GSC_OK;
+      std::vector<float4> A(ns), B(ns), Cc(ns);
+      std::vector<uint2> bx(ns);
+      CU(cudaMemcpy(A.data(), ctx->spA.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(B.data(), ctx->spB.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(Cc.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(bx.data(), ctx->box.p, ns * 8, cudaMemcpyDeviceToHost));
+      std::vector<float> out(ns * 12);
+      for (size_t k = 0; k < ns; ++k) {
+        float r[12] = {A[k].x, A[k].y, A[k].z, A[k].w, B[k].x, B[k].y, B[k].z, B[k].w, Cc[k].x, Cc[k].z, Cc[k].y,
+                       (float)(bx[k].y >> 31)};
+        std::memcpy(&out[12 * k], r, sizeof(r));
+      }
+      std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));
+      return GSC_OK;
+    }
+    default: return fail(ctx, GSC_EINVAL, "unknown debug selector");
+  }
+}
+
+gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n) {
+  if (!ctx || fn < 0 || fn > 3 || (n && (!dev_in || !dev_out))) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  launch_elem(fn, dev_in, dev_out, n, ctx->num_sms, nullptr);
+  CU(cudaGetLastError());
+  CU(cudaDeviceSynchronize());
+  return GSC_OK;
+}
+
+const char *gsc_last_error(const gsc_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+void gsc_destroy(gsc_ctx *ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaDeviceSynchronize();
+  for (auto &s : ctx->slots)
+    if (s.timed)
+      for (int k = 0; k < kEvents; ++k) cudaEventDestroy(s.ev[k]);
+  if (ctx->rec_host) cudaFreeHost(ctx->rec_host);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  delete ctx;
+}
+
+}  // extern "C"

@@ -1,0 +1,280 @@
+// gsc_internal.cuh -- product-side device types and helpers (B200 / sm_100a).
+// Shares nothing with oracle/.  Arithmetic follows DESIGN.md "Numerics";
+// every .cu is compiled with -fmad=false -prec-div=true -prec-sqrt=true
+// -ftz=false so IEEE fp32 ops are emitted exactly as written (FMA only where
+// __fmaf_rn is spelled out).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gsc {
+
+constexpr int kF = 32;       // feature dim
+constexpr int kK = 10;       // Gaussians per anchor
+constexpr int kH = 32;       // hidden width per head
+constexpr int kNOut = 11 * kK;
+constexpr int kTile = 16;    // 16x16 pixel tiles
+
+// ---- per-frame constants (host fp64 -> fp32, Eqs. 5-6) ----
+struct EyeC {
+  float p[3], r0[3], r1[3], r2[3];
+  float fx, fy, cx, cy, near_plane, far_plane, limx, limy;
+};
+struct UniC {
+  float p[3], right[3], up[3], fwd[3];
+  float near_plane, far_plane, tx, ty, kx, ky;
+};
+struct FrameC {
+  UniC u;
+  EyeC eye[2];
+  int width, height, TW, TH, Te;   // tiles per row / column / eye
+  int L;
+  float d0;
+  float bg[3];
+};
+
+// ---- device-resident counters, zeroed at every frame start ----
+struct FrameCounters {
+  uint32_t tile_cull, tile_derive, tile_project, tile_emit;
+  uint32_t tile_sort[8];
+  uint32_t n_visible, n_miss, n_new, n_splat;
+  uint32_t n_pairs_raw;        // pairs the frame needed
+  uint32_t n_pairs;            // min(raw, capacity)
+  uint32_t overflow;
+  uint32_t pad;
+  uint32_t hist_depth[4][256];
+  uint32_t hist_tile[2][256];
+};
+
+// ---- persistent cache-policy state (not reset per frame) ----
+struct PolicyState {
+  int32_t frame;       // f of the next frame
+  int32_t depth;       // depth_f in effect for the next frame
+  int32_t W;           // watermark W_f = max_{f'<=f}(f' - depth_f')
+  int32_t d_max;
+  int32_t literal;     // GSC_F_DEPTH_LITERAL
+  int32_t pad[3];
+};
+
+// compacted splat records (index c), written by project, read by emit/blend
+struct SplatBufs {
+  float4 *spA;       // (u, v, A, B)       A,B,C = conic (A dx^2 + 2B dx dy + C dy^2)
+  float4 *spB;       // (C, alpha, r, g)
+  float4 *spC;       // (b, thr, depth, 0)
+  uint2 *box;        // candidate tile box: tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
+  uint32_t *count;   // kept tiles
+  uint32_t *depth;   // depth key = bits(z) (depth-sort input)
+  uint32_t *gslot;   // Gaussian slot g
+};
+
+struct EmitIn {
+  const uint32_t *sorted;   // splat indices in depth order
+  const float4 *spA;
+  const float4 *spB;
+  const float4 *spC;
+  const uint2 *box;
+  const uint32_t *count;
+};
+
+// snapshot copied to host every frame
+struct FrameRecordDev {
+  int32_t frame, depth_used, depth_next, pad0;
+  uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, pad1, pad2;
+};
+
+// ---------------------------------------------------------------- helpers
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+__device__ __forceinline__ float f_of_u(uint32_t b) { return __uint_as_float(b); }
+__device__ __forceinline__ uint32_t u_of_f(float f) { return __float_as_uint(f); }
+
+__device__ __forceinline__ uint32_t ld_volatile_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_volatile_u64(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_volatile_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Decoupled look-back over 32-bit status words: [31:30] flag (1 = aggregate,
+// 2 = inclusive prefix), [29:0] value.  Called by one full warp; returns the
+// exclusive prefix of `tile` (identical in all lanes).
+__device__ __forceinline__ uint32_t lookback_u32(uint32_t *status, uint32_t tile) {
+  constexpr uint32_t kMask = 0x3FFFFFFFu;
+  uint32_t prefix = 0;
+  int64_t base = (int64_t)tile - 1;
+  const uint32_t lane = lane_id();
+  while (base >= 0) {
+    int64_t idx = base - (int64_t)lane;
+    uint32_t s = 2u << 30;  // out of range counts as an inclusive zero
+    if (idx >= 0) {
+      do { s = ld_volatile_u32(status + idx); } while ((s >> 30) == 0);
+    }
+    uint32_t incl = __ballot_sync(0xFFFFFFFFu, (s >> 30) == 2u);
+    uint32_t upto = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;   // nearest inclusive lane
+    uint32_t v = (lane <= upto) ? (s & kMask) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    prefix += v;
+    if (incl) break;
+    base -= 32;
+  }
+  return prefix;
+}
+
+// 64-bit status: [63:62] flag, [61:31] field b, [30:0] field a (two counts).
+__device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *status, uint32_t tile) {
+  constexpr unsigned long long kMask = (1ull << 62) - 1;
+  unsigned long long prefix = 0;
+  int64_t base = (int64_t)tile - 1;
+  const uint32_t lane = lane_id();
+  while (base >= 0) {
+    int64_t idx = base - (int64_t)lane;
+    unsigned long long s = 2ull << 62;
+    if (idx >= 0) {
+      do { s = ld_volatile_u64(status + idx); } while ((s >> 62) == 0);
+    }
+    uint32_t incl = __ballot_sync(0xFFFFFFFFu, (s >> 62) == 2ull);
+    uint32_t upto = incl ? (uint32_t)(__ffs(incl) - 1) : 31u;
+    unsigned long long v = (lane <= upto) ? (s & kMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    prefix += v;
+    if (incl) break;
+    base -= 32;
+  }
+  return prefix;
+}
+
+// ---------------------------------------------------------------- elementary functions
+// DESIGN.md Numerics N1-N4.  Independent implementation of the same op
+// sequence the oracle uses; __fmaf_rn only where the definition says fma.
+__device__ __forceinline__ float exp_s(float x) {
+  if (x != x) return x;
+  if (x > 88.72283935546875f) return __int_as_float(0x7F800000);
+  if (x < -87.33654022216797f) return 0.0f;
+  const float log2e = 1.44269502162933349609375f;
+  const float ln2_hi = 0.693145751953125f;
+  const float ln2_lo = 1.428606765330187045037746429443359375e-06f;
+  float n = rintf(__fmul_rn(x, log2e));
+  float r = __fsub_rn(x, __fmul_rn(n, ln2_hi));
+  r = __fsub_rn(r, __fmul_rn(n, ln2_lo));
+  float p = 1.98412698e-04f;
+  p = __fmaf_rn(p, r, 1.38888889e-03f);
+  p = __fmaf_rn(p, r, 8.33333377e-03f);
+  p = __fmaf_rn(p, r, 4.16666679e-02f);
+  p = __fmaf_rn(p, r, 1.66666672e-01f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  int ni = __float2int_rz(n);
+  if (ni > 127) return __fmul_rn(__fmul_rn(p, __uint_as_float(0x7F000000u)), 2.0f);
+  return __fmul_rn(p, __uint_as_float((uint32_t)(ni + 127) << 23));
+}
+
+__device__ __forceinline__ float log_s(float x) {
+  if (x != x) return x;
+  if (x < 0.0f) return __int_as_float(0x7FC00000);
+  if (x == 0.0f) return __int_as_float(0xFF800000);
+  if (x == __int_as_float(0x7F800000)) return x;
+  uint32_t b = __float_as_uint(x);
+  int k = 0;
+  if (b < 0x00800000u) { x = __fmul_rn(x, 8388608.0f); b = __float_as_uint(x); k = -23; }
+  k += (int)(b >> 23) - 127;
+  float m = __uint_as_float((b & 0x007FFFFFu) | 0x3F800000u);
+  if (m > 1.41421353816986083984375f) { m = __fmul_rn(m, 0.5f); k += 1; }
+  float f = __fsub_rn(m, 1.0f);
+  float s = __fdiv_rn(f, __fadd_rn(2.0f, f));
+  float z = __fmul_rn(s, s);
+  float R = __fmaf_rn(z, 0.222222222f, 0.285714298f);
+  R = __fmaf_rn(z, R, 0.400000006f);
+  R = __fmaf_rn(z, R, 0.666666687f);
+  R = __fmul_rn(z, R);
+  float hfsq = __fmul_rn(0.5f, __fmul_rn(f, f));
+  float dk = __int2float_rn(k);
+  const float ln2_hi = 0.693145751953125f;
+  const float ln2_lo = 1.428606765330187045037746429443359375e-06f;
+  float inner = __fadd_rn(__fmul_rn(s, __fadd_rn(hfsq, R)), __fmul_rn(dk, ln2_lo));
+  float lg = __fsub_rn(f, __fsub_rn(hfsq, inner));
+  return __fadd_rn(__fmul_rn(dk, ln2_hi), lg);
+}
+
+__device__ __forceinline__ float tanh_s(float x) {
+  if (x != x) return x;
+  float a = fabsf(x);
+  float r;
+  if (a < 0.5f) {
+    float z = __fmul_rn(a, a);
+    float p = 5.90027440e-04f;
+    p = __fmaf_rn(p, z, -1.45583438e-03f);
+    p = __fmaf_rn(p, z, 3.59212872e-03f);
+    p = __fmaf_rn(p, z, -8.86323553e-03f);
+    p = __fmaf_rn(p, z, 2.18694885e-02f);
+    p = __fmaf_rn(p, z, -5.39682540e-02f);
+    p = __fmaf_rn(p, z, 1.33333340e-01f);
+    p = __fmaf_rn(p, z, -3.33333343e-01f);
+    r = __fmaf_rn(__fmul_rn(a, z), p, a);
+  } else {
+    float e = exp_s(__fmul_rn(2.0f, a));
+    r = __fsub_rn(1.0f, __fdiv_rn(2.0f, __fadd_rn(e, 1.0f)));
+  }
+  return copysignf(r, x);
+}
+
+__device__ __forceinline__ float sigmoid_s(float x) {
+  return __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_s(-x)));
+}
+
+// exact dot product in the written order ((a0 b0 + a1 b1) + a2 b2)
+__device__ __forceinline__ float dot3(float a0, float a1, float a2, const float *b) {
+  return __fadd_rn(__fadd_rn(__fmul_rn(a0, b[0]), __fmul_rn(a1, b[1])), __fmul_rn(a2, b[2]));
+}
+
+// floor(log2(x)) of a positive finite or infinite float, from its bits
+__device__ __forceinline__ int ilogb_bits(float x) {
+  uint32_t b = __float_as_uint(x) & 0x7FFFFFFFu;
+  if (b >= 0x7F800000u) return 0x7FFFFFFF;                // inf / nan
+  if (b >= 0x00800000u) return (int)(b >> 23) - 127;      // normal
+  return -127 - (__clz(b) - 9);                           // subnormal: 2^-126 * 0.m
+}
+
+// ---- the exact tile test (O-5 R14), shared by project and emit ----
+constexpr float kKappa = 1.0009765625f;   // 1 + 2^-10
+constexpr float kSlack = 0.015625f;       // 2^-6
+constexpr float kAlphaMin = 0.0039215688593685626983642578125f;  // fp32(1/255)
+
+__device__ __forceinline__ float edge_q(float d, float lo, float hi, float P, float Q, float R) {
+  float t = __fdiv_rn(-__fmul_rn(Q, d), R);
+  t = fminf(fmaxf(t, lo), hi);
+  return __fadd_rn(__fadd_rn(__fmul_rn(P, __fmul_rn(d, d)), __fmul_rn(2.0f, __fmul_rn(Q, __fmul_rn(d, t)))),
+                   __fmul_rn(R, __fmul_rn(t, t)));
+}
+
+__device__ __forceinline__ bool tile_kept(float u, float v, float A, float B, float C, float thr, int tx, int ty,
+                                          int width, int height) {
+  int px1 = min(16 * tx + 15, width - 1), py1 = min(16 * ty + 15, height - 1);
+  float X0 = __fadd_rn((float)(16 * tx), 0.5f), X1 = __fadd_rn((float)px1, 0.5f);
+  float Y0 = __fadd_rn((float)(16 * ty), 0.5f), Y1 = __fadd_rn((float)py1, 0.5f);
+  if (u >= X0 && u <= X1 && v >= Y0 && v <= Y1) return true;  // q_min = 0 <= thr
+  float dx0 = __fsub_rn(X0, u), dx1 = __fsub_rn(X1, u), dy0 = __fsub_rn(Y0, v), dy1 = __fsub_rn(Y1, v);
+  float q = edge_q(dx0, dy0, dy1, A, B, C);
+  q = fminf(q, edge_q(dx1, dy0, dy1, A, B, C));
+  q = fminf(q, edge_q(dy0, dx0, dx1, C, B, A));
+  q = fminf(q, edge_q(dy1, dx0, dx1, C, B, A));
+  return q <= thr;
+}
+
+}  // namespace gsc

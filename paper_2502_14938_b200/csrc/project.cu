@@ -1,0 +1,214 @@
+// project.cu -- SURVEY §8(a) row a4: EWA projection,
+// opacity-aware extent r^2 = 2 ln(255 alpha) ("considering the opacity
+// can scale down the size of the ellipse") and the exact
+// tile-coverage count (FlashGS citation), both eyes batched
+// ("independently or in batching"; R19).
+//
+// One thread per visible slot s = v*K + j (Gaussian g = X_f[v]*K + j),
+// 2 slots per thread, 512 slots per tile.  A dead slot costs its 4-byte alpha
+// read; a live one adds its 48-byte pool record.  Splats with >= 1 kept tile
+// are compacted in (eye, s) order -- the order that makes the later stable
+// sorts break depth ties by g like the oracle -- with a decoupled look-back.
+// Also fused: the 4 x 256-bin digit histogram of the depth keys (first pass
+// of the onesweep depth sort) and the pair count.
+#include "gsc_internal.cuh"
+
+namespace gsc {
+
+constexpr int kPThreads = 256;
+constexpr int kPItems = 2;
+constexpr int kPTile = kPThreads * kPItems;
+
+struct SplatOut {
+  float u, v, A, B, C, thr;
+  uint32_t box_x, box_y;   // tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
+  uint32_t n;
+  float depth;
+};
+
+__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float alpha,
+                                            const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
+  float rho = __fmul_rn(255.0f, alpha);
+  if (!(rho > 1.0f)) return false;
+  float t0 = __fsub_rn(p0.x, ec.p[0]), t1 = __fsub_rn(p0.y, ec.p[1]), t2 = __fsub_rn(p0.z, ec.p[2]);
+  float x = dot3(t0, t1, t2, ec.r0), y = dot3(t0, t1, t2, ec.r1), z = dot3(t0, t1, t2, ec.r2);
+  if (!(z > ec.near_plane) || z > ec.far_plane) return false;
+  float xz = __fdiv_rn(x, z), yz = __fdiv_rn(y, z);
+  float xc = __fmul_rn(fminf(fmaxf(xz, -ec.limx), ec.limx), z);
+  float yc = __fmul_rn(fminf(fmaxf(yz, -ec.limy), ec.limy), z);
+  float zz = __fmul_rn(z, z);
+  float J00 = __fdiv_rn(ec.fx, z), J02 = __fdiv_rn(-__fmul_rn(ec.fx, xc), zz);
+  float J11 = __fdiv_rn(ec.fy, z), J12 = __fdiv_rn(-__fmul_rn(ec.fy, yc), zz);
+  float T[2][3];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    T[0][k] = __fadd_rn(__fmul_rn(J00, ec.r0[k]), __fmul_rn(J02, ec.r2[k]));
+    T[1][k] = __fadd_rn(__fmul_rn(J11, ec.r1[k]), __fmul_rn(J12, ec.r2[k]));
+  }
+  // Sigma (00 01 02 11 12 22) = (p0.w, p1.x, p1.y, p1.z, p1.w, p2.x)
+  const float S[3][3] = {{p0.w, p1.x, p1.y}, {p1.x, p1.z, p1.w}, {p1.y, p1.w, p2.x}};
+  float U[2][3];
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int k = 0; k < 3; ++k)
+      U[r][k] = __fadd_rn(__fadd_rn(__fmul_rn(T[r][0], S[0][k]), __fmul_rn(T[r][1], S[1][k])),
+                          __fmul_rn(T[r][2], S[2][k]));
+  float a = dot3(U[0][0], U[0][1], U[0][2], T[0]);
+  float b = dot3(U[0][0], U[0][1], U[0][2], T[1]);
+  float c = dot3(U[1][0], U[1][1], U[1][2], T[1]);
+  a = __fadd_rn(a, 0.3f);
+  c = __fadd_rn(c, 0.3f);
+  float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));
+  if (!(det > 0.0f)) return false;
+  o.A = __fdiv_rn(c, det);
+  o.B = __fdiv_rn(-b, det);
+  o.C = __fdiv_rn(a, det);
+  o.u = __fadd_rn(__fmul_rn(ec.fx, xz), ec.cx);
+  o.v = __fadd_rn(__fmul_rn(ec.fy, yz), ec.cy);
+  float r2 = __fmul_rn(2.0f, log_s(rho));
+  o.thr = __fadd_rn(__fmul_rn(r2, kKappa), kSlack);
+  o.depth = z;
+  if (!isfinite(o.A) || !isfinite(o.B) || !isfinite(o.C) || !isfinite(o.u) || !isfinite(o.v) || !isfinite(o.thr))
+    return false;
+  float ex = __fadd_rn(__fsqrt_rn(__fmul_rn(o.thr, a)), 1.0f), ey = __fadd_rn(__fsqrt_rn(__fmul_rn(o.thr, c)), 1.0f);
+  float fx0 = fmaxf(floorf(__fmul_rn(__fsub_rn(o.u, ex), 0.0625f)), 0.0f);
+  float fx1 = fminf(floorf(__fmul_rn(__fadd_rn(o.u, ex), 0.0625f)), (float)(TW - 1));
+  float fy0 = fmaxf(floorf(__fmul_rn(__fsub_rn(o.v, ey), 0.0625f)), 0.0f);
+  float fy1 = fminf(floorf(__fmul_rn(__fadd_rn(o.v, ey), 0.0625f)), (float)(TH - 1));
+  if (fx0 > fx1 || fy0 > fy1) return false;
+  int tx0 = (int)fx0, tx1 = (int)fx1, ty0 = (int)fy0, ty1 = (int)fy1;
+  uint32_t n = 0;
+  for (int ty = ty0; ty <= ty1; ++ty)
+    for (int tx = tx0; tx <= tx1; ++tx) n += tile_kept(o.u, o.v, o.A, o.B, o.C, o.thr, tx, ty, width, height);
+  o.n = n;
+  o.box_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
+  o.box_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
+  return n > 0;
+}
+
+__global__ void __launch_bounds__(kPThreads)
+project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__restrict__ alpha,
+               const float4 *__restrict__ pool, SplatBufs sb, uint32_t *__restrict__ status,
+               FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ uint32_t s_cnt[2][kPItems][kPThreads / 32];
+  __shared__ uint32_t s_hist[4][256];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
+  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
+  const uint32_t S = ctr->n_visible * (uint32_t)kK;
+  const uint32_t ntiles = (S + kPTile - 1) / kPTile;
+  uint32_t pairs_local = 0;
+
+  for (;;) {
+    __syncthreads();
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_project, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+
+    SplatOut so[kPItems][2];
+    bool ok[kPItems][2];
+    uint32_t gs[kPItems];
+    float4 q0[kPItems], q1[kPItems], q2[kPItems];
+    float al[kPItems];
+#pragma unroll
+    for (int it = 0; it < kPItems; ++it) {
+      uint32_t s = tile * kPTile + it * kPThreads + warp * 32 + lane;
+      ok[it][0] = ok[it][1] = false;
+      al[it] = 0.0f;
+      gs[it] = 0;
+      if (s < S) {
+        uint32_t v = s / kK, j = s - v * kK;
+        uint32_t g = visible[v] * kK + j;
+        gs[it] = g;
+        al[it] = alpha[g];
+        if (__fmul_rn(255.0f, al[it]) > 1.0f) {
+          q0[it] = pool[3 * (size_t)g];
+          q1[it] = pool[3 * (size_t)g + 1];
+          q2[it] = pool[3 * (size_t)g + 2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0[it], q1[it], q2[it],
+                                    so[it][e]);
+        }
+      }
+    }
+    uint32_t m[2][kPItems];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int it = 0; it < kPItems; ++it) {
+        m[e][it] = __ballot_sync(0xFFFFFFFFu, ok[it][e]);
+        if (lane == 0) s_cnt[e][it][warp] = __popc(m[e][it]);
+        if (ok[it][e]) pairs_local += so[it][e].n;
+      }
+    __syncthreads();
+    if (warp == 0) {
+      // exclusive scan over the 2 * kPItems * 8 = 32 counts in (eye, item, warp) order
+      uint32_t c = (&s_cnt[0][0][0])[lane];
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t tv = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += tv;
+      }
+      uint32_t agg = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      (&s_cnt[0][0][0])[lane] = inc - c;
+      uint32_t pre = 0;
+      if (tile == 0) {
+        if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
+      } else {
+        if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
+        pre = lookback_u32(status, tile);
+        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+      }
+      if (lane == 0) {
+        s_prefix = pre;
+        if (tile == ntiles - 1) ctr->n_splat = pre + agg;
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int it = 0; it < kPItems; ++it) {
+        if (!ok[it][e]) continue;
+        const SplatOut &o = so[it][e];
+        uint32_t c = s_prefix + s_cnt[e][it][warp] + __popc(m[e][it] & lt);
+        sb.spA[c] = make_float4(o.u, o.v, o.A, o.B);
+        sb.spB[c] = make_float4(o.C, al[it], q2[it].y, q2[it].z);
+        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
+        sb.count[c] = o.n;
+        uint32_t dk = __float_as_uint(o.depth);
+        sb.spC[c] = make_float4(q2[it].w, o.thr, __uint_as_float(dk), 0.0f);
+        sb.depth[c] = dk;
+        sb.gslot[c] = gs[it];
+#pragma unroll
+        for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
+      }
+  }
+  // flush the fused histogram and the pair count
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) {
+    uint32_t v = (&s_hist[0][0])[k];
+    if (v) atomicAdd(&ctr->hist_depth[0][0] + k, v);
+  }
+  for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
+  if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
+}
+
+static int g_project_grid = 0;
+
+void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
+                    const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms, cudaStream_t st) {
+  if (g_project_grid == 0) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel, kPThreads, 0);
+    g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  }
+  project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, visible, alpha, pool, sb, status, ctr);
+}
+int project_tile_size() { return kPTile; }
+
+}  // namespace gsc

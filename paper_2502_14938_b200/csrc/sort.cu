@@ -1,0 +1,329 @@
+// sort.cu -- SURVEY §8(a) rows a5 (key duplication), a6 (radix sort by
+// (tile, depth)) and a7 (tile ranges).
+//
+// The (tile, depth) order is produced as an LSD radix sort whose depth digits
+// run BEFORE duplication: the splats are first stably sorted by their 32-bit
+// depth key (4 onesweep passes over one key per splat), then duplicated into
+// (tile, splat) pairs in depth order ("key-value pairs"), then stably
+// sorted by the 14-bit tile id (2 onesweep passes).  Stability of every pass
+// makes the result identical to one sort of 46-bit (tile << 32 | depth) keys
+// with ties broken by the Gaussian slot g (the oracle's order), while moving
+// ~2.5x fewer bytes than duplicating first.
+//
+// Onesweep pass (Adinets & Merrill 2022 style): one kernel per 8-bit digit;
+// tiles of 4096 keys acquired in launch order through an atomic counter;
+// stable block-local ranking by warp match_any; per-digit decoupled look-back
+// across tiles; scatter through shared memory for coalesced writes.  The
+// global digit histograms come fused from the producing kernel (project for
+// depth keys, emit for tile keys).  Look-back status words live in two
+// buffers that alternate between passes; each pass clears the other buffer's
+// entries for the tiles it owns, so no per-sort memset is needed (an even
+// number of passes leaves buffer A clean).
+#include "gsc_internal.cuh"
+
+namespace gsc {
+
+constexpr int kSThreads = 256;
+constexpr int kSWarps = kSThreads / 32;
+constexpr int kSItems = 16;
+constexpr int kSTile = kSThreads * kSItems;   // 4096 keys
+constexpr int kBins = 256;
+
+struct SortSmem {
+  uint32_t keys[kSTile];
+  uint32_t vals[kSTile];
+  uint32_t whist[kSWarps][kBins + 4];   // per-warp counts -> exclusive prefixes (bin 256 = invalid)
+  uint32_t blk_off[kBins];
+  uint32_t gbase[kBins];
+  uint32_t tile;
+};
+
+template <bool kIota>
+__global__ void __launch_bounds__(kSThreads)
+onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
+                     uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                     const uint32_t *__restrict__ d_count, uint32_t shift, const uint32_t *__restrict__ hist,
+                     uint32_t *__restrict__ status, uint32_t *__restrict__ status_clear,
+                     uint32_t *__restrict__ tile_ctr) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SortSmem &S = *reinterpret_cast<SortSmem *>(smem_raw);
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id(), lt = lanemask_lt();
+  const uint32_t n = *d_count;
+  const uint32_t ntiles = (n + kSTile - 1) / kSTile;
+
+  // exclusive scan of this pass's global digit histogram (every block, once)
+  __shared__ uint32_t s_hex[kBins];
+  {
+    uint32_t h = hist[t];
+    uint32_t inc = h;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= (uint32_t)o) inc += v;
+    }
+    __shared__ uint32_t s_w[kSWarps];
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    uint32_t wp = 0;
+    for (uint32_t w = 0; w < warp; ++w) wp += s_w[w];
+    s_hex[t] = wp + inc - h;
+  }
+
+  for (;;) {
+    __syncthreads();
+    if (t == 0) S.tile = atomicAdd(tile_ctr, 1u);
+    for (int k = t; k < kSWarps * (kBins + 4); k += kSThreads) (&S.whist[0][0])[k] = 0;
+    __syncthreads();
+    const uint32_t tile = S.tile;
+    if (tile >= ntiles) break;
+    const uint32_t wbase = tile * kSTile + warp * (32 * kSItems);
+
+    uint32_t key[kSItems], rank[kSItems];
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      uint32_t idx = wbase + i * 32 + lane;
+      key[i] = idx < n ? keys_in[idx] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      uint32_t idx = wbase + i * 32 + lane;
+      uint32_t d = idx < n ? (key[i] >> shift) & 0xFFu : (uint32_t)kBins;
+      uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
+      uint32_t before = S.whist[warp][d];
+      rank[i] = before + __popc(peers & lt);
+      __syncwarp();
+      if (lane == (uint32_t)(__ffs(peers) - 1)) S.whist[warp][d] = before + __popc(peers);
+      __syncwarp();
+    }
+    __syncthreads();
+
+    // per digit: exclusive prefix over warps, tile count, publish + look back
+    {
+      const uint32_t d = t;
+      uint32_t run = 0;
+#pragma unroll
+      for (int w = 0; w < kSWarps; ++w) {
+        uint32_t c = S.whist[w][d];
+        S.whist[w][d] = run;
+        run += c;
+      }
+      uint32_t *st = status + (size_t)tile * kBins + d;
+      uint32_t pre = 0;
+      if (tile == 0) {
+        st_volatile_u32(st, (2u << 30) | run);
+      } else {
+        st_volatile_u32(st, (1u << 30) | run);
+        int64_t p = (int64_t)tile - 1;
+        while (p >= 0) {
+          uint32_t s;
+          do { s = ld_volatile_u32(status + (size_t)p * kBins + d); } while ((s >> 30) == 0);
+          pre += s & 0x3FFFFFFFu;
+          if ((s >> 30) == 2u) break;
+          --p;
+        }
+        st_volatile_u32(st, (2u << 30) | (pre + run));
+      }
+      status_clear[(size_t)tile * kBins + d] = 0u;
+      S.gbase[d] = s_hex[d] + pre;
+      // block-local exclusive scan of tile counts over digits
+      uint32_t inc = run;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += v;
+      }
+      __shared__ uint32_t s_w2[kSWarps];
+      if (lane == 31) s_w2[warp] = inc;
+      __syncthreads();
+      uint32_t wp = 0;
+      for (uint32_t w = 0; w < warp; ++w) wp += s_w2[w];
+      S.blk_off[d] = wp + inc - run;
+    }
+    __syncthreads();
+
+    // scatter into shared memory in (digit, original order)
+#pragma unroll
+    for (int i = 0; i < kSItems; ++i) {
+      uint32_t idx = wbase + i * 32 + lane;
+      if (idx < n) {
+        uint32_t d = (key[i] >> shift) & 0xFFu;
+        uint32_t pos = S.blk_off[d] + S.whist[warp][d] + rank[i];
+        S.keys[pos] = key[i];
+        S.vals[pos] = kIota ? idx : vals_in[idx];
+      }
+    }
+    __syncthreads();
+    const uint32_t nvalid = min((uint32_t)kSTile, n - tile * kSTile);
+    for (uint32_t i = t; i < nvalid; i += kSThreads) {
+      uint32_t k = S.keys[i];
+      uint32_t d = (k >> shift) & 0xFFu;
+      uint32_t o = S.gbase[d] + (i - S.blk_off[d]);
+      keys_out[o] = k;
+      vals_out[o] = S.vals[i];
+    }
+  }
+}
+
+// ------------------------------------------------------------------ emit (a5)
+// Pairs (tile, splat) in depth order: sorted position p -> splat c; exclusive
+// scan of the kept-tile counts (decoupled look-back); the exact tile test of
+// project is re-evaluated to enumerate the kept tiles (identical arithmetic).
+constexpr int kEThreads = 256;
+constexpr int kEItems = 4;
+constexpr int kETile = kEThreads * kEItems;
+
+__global__ void __launch_bounds__(kEThreads)
+emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint32_t *__restrict__ keys_out,
+            uint32_t *__restrict__ vals_out, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_tile, s_prefix, s_w[kEThreads / 32];
+  __shared__ uint32_t s_hist[2][256];
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id();
+  for (int k = t; k < 512; k += kEThreads) (&s_hist[0][0])[k] = 0;
+  const uint32_t C = ctr->n_splat;
+  const uint32_t ntiles = (C + kETile - 1) / kETile;
+  for (;;) {
+    __syncthreads();
+    if (t == 0) s_tile = atomicAdd(&ctr->tile_emit, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    const uint32_t p0 = tile * kETile + t * kEItems;
+    uint32_t c[kEItems], cnt[kEItems], sum = 0;
+#pragma unroll
+    for (int i = 0; i < kEItems; ++i) {
+      uint32_t p = p0 + i;
+      c[i] = p < C ? in.sorted[p] : 0u;
+      cnt[i] = p < C ? in.count[c[i]] : 0u;
+      sum += cnt[i];
+    }
+    uint32_t inc = sum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= (uint32_t)o) inc += v;
+    }
+    if (lane == 31) s_w[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+      uint32_t wv = lane < kEThreads / 32 ? s_w[lane] : 0u, wi = wv;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
+        if (lane >= (uint32_t)o) wi += v;
+      }
+      uint32_t agg = __shfl_sync(0xFFFFFFFFu, wi, 31);
+      if (lane < kEThreads / 32) s_w[lane] = wi - wv;
+      uint32_t pre = 0;
+      if (tile == 0) {
+        if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
+      } else {
+        if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
+        pre = lookback_u32(status, tile);
+        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+      }
+      if (lane == 0) {
+        s_prefix = pre;
+        if (tile == ntiles - 1) {
+          uint32_t tot = pre + agg;
+          ctr->n_pairs = tot < cap ? tot : cap;
+          ctr->overflow = tot > cap;
+        }
+      }
+    }
+    __syncthreads();
+    uint32_t off = s_prefix + s_w[warp] + inc - sum;
+#pragma unroll
+    for (int i = 0; i < kEItems; ++i) {
+      if (cnt[i] == 0) continue;
+      const uint32_t ci = c[i];
+      const float4 a = in.spA[ci];
+      const float Cc = in.spB[ci].x;
+      const float thr = in.spC[ci].y;
+      const uint2 bx = in.box[ci];
+      const int tx0 = bx.x & 0xFFFF, tx1 = bx.x >> 16, ty0 = bx.y & 0xFFFF, ty1 = (bx.y >> 16) & 0x7FFF;
+      const uint32_t ebase = (bx.y >> 31) ? (uint32_t)Te : 0u;
+      for (int ty = ty0; ty <= ty1; ++ty)
+        for (int tx = tx0; tx <= tx1; ++tx)
+          if (tile_kept(a.x, a.y, a.z, a.w, Cc, thr, tx, ty, width, height)) {
+            uint32_t key = ebase + (uint32_t)(ty * TW + tx);
+            if (off < cap) {
+              keys_out[off] = key;
+              vals_out[off] = ci;
+              atomicAdd(&s_hist[0][key & 0xFFu], 1u);
+              atomicAdd(&s_hist[1][(key >> 8) & 0xFFu], 1u);
+            }
+            ++off;
+          }
+    }
+  }
+  __syncthreads();
+  for (int k = t; k < 512; k += kEThreads) {
+    uint32_t v = (&s_hist[0][0])[k];
+    if (v) atomicAdd(&ctr->hist_tile[0][0] + k, v);
+  }
+}
+
+// ------------------------------------------------------------------ ranges (a7)
+__global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *__restrict__ ctr,
+                              uint2 *__restrict__ ranges) {
+  const uint32_t P = ctr->n_pairs;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    uint32_t k = keys[p];
+    if (p == 0 || keys[p - 1] != k) ranges[k].x = p;
+    if (p == P - 1 || keys[p + 1] != k) ranges[k].y = p + 1;
+  }
+}
+
+// ------------------------------------------------------------------ launchers
+static int g_sort_grid = 0, g_emit_grid = 0;
+
+static void sort_setup(int num_sms) {
+  if (g_sort_grid) return;
+  const int smem = (int)sizeof(SortSmem);
+  cudaFuncSetAttribute(onesweep_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(onesweep_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  int per_sm = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pass_kernel<false>, kSThreads, smem);
+  g_sort_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+}
+
+// Sort `passes` (even) 8-bit digits (shift 0, 8, ...) of keys_a[0..*d_count)
+// with payloads vals_a (iota payloads when `iota`).  Ping-pongs a -> b -> a;
+// with an even pass count the result lands back in keys_a / vals_a.
+void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, bool iota,
+                     const uint32_t *d_count, int passes, const uint32_t *hist /* [passes][256] */,
+                     uint32_t *status_a, uint32_t *status_b, uint32_t *tile_ctrs, int num_sms, cudaStream_t st) {
+  sort_setup(num_sms);
+  const int smem = (int)sizeof(SortSmem);
+  for (int p = 0; p < passes; ++p) {
+    const bool odd = p & 1;
+    uint32_t *ki = odd ? keys_b : keys_a, *vi = odd ? vals_b : vals_a;
+    uint32_t *ko = odd ? keys_a : keys_b, *vo = odd ? vals_a : vals_b;
+    uint32_t *stc = odd ? status_b : status_a, *stx = odd ? status_a : status_b;
+    if (p == 0 && iota)
+      onesweep_pass_kernel<true><<<g_sort_grid, kSThreads, smem, st>>>(ki, nullptr, ko, vo, d_count, 8u * p,
+                                                                        hist + 256 * p, stc, stx, tile_ctrs + p);
+    else
+      onesweep_pass_kernel<false><<<g_sort_grid, kSThreads, smem, st>>>(ki, vi, ko, vo, d_count, 8u * p,
+                                                                         hist + 256 * p, stc, stx, tile_ctrs + p);
+  }
+}
+
+void launch_emit(const EmitIn &in, int width, int height, int TW, int Te, uint32_t cap, uint32_t *keys_out,
+                 uint32_t *vals_out, uint32_t *status, FrameCounters *ctr, int num_sms, cudaStream_t st) {
+  if (!g_emit_grid) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel, kEThreads, 0);
+    g_emit_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  }
+  emit_kernel<<<g_emit_grid, kEThreads, 0, st>>>(in, width, height, TW, Te, cap, keys_out, vals_out, status, ctr);
+}
+
+void launch_ranges(const uint32_t *keys, const FrameCounters *ctr, uint2 *ranges, int num_sms, cudaStream_t st) {
+  ranges_kernel<<<num_sms * 4, 256, 0, st>>>(keys, ctr, ranges);
+}
+
+int sort_tile_size() { return kSTile; }
+int emit_tile_size() { return kETile; }
+
+}  // namespace gsc

@@ -1,0 +1,150 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (BASELINE.json configs)."""
+import numpy as np
+import pytest
+
+import scenegen as sg
+from parity import (compare_images, compare_pool, compare_sets, compare_splats_pairs, oracle_config,
+                    renderer)
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _frame_parity(orc, o, r, rig, full=True, images=True):
+    res = o.frame(rig, raster=full, images=images and full)
+    gl, gr, st = r.render(rig)
+    vis, mis = compare_sets(o, r, st)
+    assert st["depth_used"] == res.stats.depth_used and st["depth_next"] == res.stats.depth_next
+    if not full:
+        return st, None
+    compare_pool(o, r, vis)
+    compare_splats_pairs(o, r)
+    d = None
+    if images:
+        d = compare_images(gl.cpu().numpy(), gr.cpu().numpy(), res.img_l, res.img_r)
+    return st, d
+
+
+def test_c1_all_poses(orc, c1):
+    """configs[0]: 1k anchors x K=10, 64x64, 4 poses; every intermediate bit-exact."""
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    for rig in sg.trajectory(cfg):
+        st, d = _frame_parity(orc, o, r, rig)
+        assert d == 0.0
+
+
+def test_c1_brute_force_pixels(orc, c1):
+    """GPU pixels equal the oracle's per-pixel brute-force (O1) renderer."""
+    cfg, sc = c1
+    for rig in sg.trajectory(cfg):
+        o = orc.Oracle(sc, oracle_config(orc, cfg))
+        res = o.frame(rig, brute=True)
+        r = renderer(cfg).load(sc)
+        gl, gr, _ = r.render(rig)
+        compare_images(gl.cpu().numpy(), gr.cpu().numpy(), res.img_l, res.img_r)
+
+
+def test_c1_moving_trajectory_cache(orc, c1):
+    """Cache state machine over a moving trajectory with D_max = 4: hit/miss sets,
+    depths and images match every frame."""
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg, d_max=4))
+    r = renderer(cfg, d_max=4).load(sc)
+    c = cfg.center
+    for f in range(24):
+        eye = c + np.array([25 * np.cos(0.12 * f), 25 * np.sin(0.12 * f), 2.0 + 0.5 * f])
+        rig = sg.look_at_rig(eye, c + np.array([0, 0, 3.0]), 0.064)
+        _frame_parity(orc, o, r, rig)
+
+
+def test_c1_spec_literal_depth(orc, c1):
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg, literal=True))
+    r = renderer(cfg, flags=gp.GSC_F_DEPTH_LITERAL).load(sc)
+    rig = sg.trajectory(cfg)[0]
+    for f in range(13):
+        _frame_parity(orc, o, r, rig, full=(f % 5 == 0))
+
+
+def test_reset_and_empty_frames(orc, c1):
+    """Edge cases: a pose seeing nothing (V = 0, no splats, no pairs -> background),
+    then reset_cache restarts at frame 0."""
+    cfg, sc = c1
+    r = renderer(cfg).load(sc)
+    eye = cfg.center + np.array([0.0, -200.0, 3.0])
+    away = sg.look_at_rig(eye, eye + np.array([0.0, -1.0, 0.0]), 0.0)
+    gl, gr, st = r.render(away)
+    assert st["n_visible"] == 0 and st["n_splats"] == 0 and st["n_pairs"] == 0
+    assert float(gl.abs().max()) == 0.0
+    r.reset_cache()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    _frame_parity(orc, o, r, sg.trajectory(cfg)[0])
+
+
+@pytest.mark.parametrize("fn,lo,hi,step", [("exp", -90.0, 90.0, 1), ("log", 1e-30, 1e30, 3),
+                                           ("tanh", -20.0, 20.0, 3), ("sigmoid", -90.0, 90.0, 3)])
+def test_elementary_functions_bitwise(orc, fn, lo, hi, step):
+    """Device exp_s/log_s/tanh_s/sigmoid_s equal the oracle's on every float of
+    the range (every `step`-th bit pattern)."""
+    import torch
+    import paper_2502_14938_b200 as gp
+    r = gp.Renderer(0, 64, 64)
+    nbad = 0
+    for sign_lo, sign_hi in ((lo, min(hi, -0.0)), (max(lo, 0.0), hi)):
+        if sign_lo > sign_hi or (sign_lo == sign_hi == 0):
+            continue
+        a = np.float32(sign_lo).view(np.uint32).astype(np.int64)
+        b = np.float32(sign_hi).view(np.uint32).astype(np.int64)
+        a, b = min(a, b), max(a, b)
+        for s0 in range(a, b + 1, 1 << 26):
+            bits = np.arange(s0, min(b + 1, s0 + (1 << 26)), step, dtype=np.int64).astype(np.uint32)
+            x = bits.view(np.float32)
+            ref = orc.elem(fn, x)
+            got = r.elementary(fn, torch.from_numpy(x).cuda()).cpu().numpy()
+            same = (got.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(got) & np.isnan(ref))
+            nbad += int((~same).sum())
+    assert nbad == 0
+
+
+# ---------------------------------------------------------------- configs[1..2] (100k, 2K binocular)
+@pytest.fixture(scope="module")
+def c100k():
+    cfg = sg.config("C3")
+    return cfg, cfg.scene()
+
+
+def test_c2_static_no_reuse(orc, c100k):
+    """configs[1]: 100k anchors, 1920x1080 binocular, static poses, D_max = 1:
+    full parity on the first frame of each static pose, sets on the others."""
+    cfg3, sc = c100k
+    cfg = sg.config("C2")
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg, n_frames=8)
+    for f, rig in enumerate(traj):
+        st, d = _frame_parity(orc, o, r, rig, full=(f in (0, 4)))
+        assert st["n_misses"] == st["n_visible"]   # D_max = 1: no reuse
+
+
+def test_c3_trajectory_reuse(orc, c100k):
+    """configs[2]: 300-frame orbit with reuse (D_max = 10): hit/miss sets and
+    depths bit-exact on every frame; full parity (pool, splats, sorted keys,
+    pixels) on frames 0, 1, 150 and 299."""
+    cfg, sc = c100k
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    hits = 0
+    for f, rig in enumerate(sg.trajectory(cfg)):
+        st, d = _frame_parity(orc, o, r, rig, full=f in (0, 1, 150, 299))
+        hits += st["n_hits"]
+    assert hits > 0
