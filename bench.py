@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""bench.py -- binocular 2K frames/s of the GS-Cache per-frame hot path.
+
+A "step" is one binocular frame: one pass of SURVEY §8(a) rows a1..a8 (cull +
+classify, depth policy, derive misses, project, depth sort, key duplication,
+tile sort, ranges, blend both eyes) over the next pose of the trajectory.
+
+Default workload (BASELINE.json configs[3], "C4"): 1M-anchor synthetic city
+block, 1920x1080 per eye, the 600-frame ground-to-aerial trajectory, D_max 10.
+N GPUs (torchrun): scene replicated, each rank renders a contiguous block of
+frames with its own cache (weak scaling: K frames per rank).  Timing: W warm-up
+frames, cache reset, then exactly K frames between a barrier + synchronise,
+CUDA events on the rendering stream, max over ranks.  The per-frame working
+set (~1-2 GB of pool / splat / pair traffic) exceeds the 126 MB L2, so no
+explicit flush is done.
+
+--impl reference: the CPU oracle (test infrastructure, oracle/) timed on the
+host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "binocular 2K frames/s"
+UNIT = "frames/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "sm_max_mhz": float(p.get("sm_max_mhz", 1965.0)),
+                "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.p = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.p.terminate()
+        self.p.wait()
+        self.f.flush()
+        self.f.seek(0)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[4:8]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _stage_bytes(s, N, K, W, H, fmt_bytes):
+    """Algorithmic HBM bytes per stage for one frame."""
+    V, M, C, P = s["n_visible"], s["n_misses"], s["n_splats"], s["n_pairs"]
+    return {
+        "cull": N * (16 + 1 + 4) + N / 4.0 + 4 * V + 8 * M,
+        "derive": M * (4 + 16 + 32 + 120 + 12) + M * K * (4 + 48),
+        "project": 4 * V + 4 * V * K + 48 * (C / 2.0) + C * (16 * 3 + 8 + 4 * 3),
+        "depth_sort": 12 * C + 3 * 16 * C,
+        "emit": C * (4 + 4 + 16 + 4 + 16 + 8) + 8 * P,
+        "tile_sort": 2 * 16 * P,
+        "ranges": 4 * P,
+        "blend": 4 * P + 36 * P + 2 * W * H * fmt_bytes,
+    }
+
+
+def run_gsc(args):
+    import torch
+    import scenegen as sg
+    import paper_2502_14938_b200 as gp
+    from paper_2502_14938_b200 import multi
+
+    rank, world, local = multi.init()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    cfg = sg.config(args.config)
+    sc = cfg.scene()
+    traj = sg.trajectory(cfg)
+    fmt = gp.GSC_FMT_RGBA8
+    r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
+                    flags=gp.GSC_F_STAGE_TIMING, pair_capacity=args.pair_capacity).load(sc)
+    out_l, out_r = r.alloc_outputs(fmt)
+    stream = torch.cuda.current_stream(dev)
+    frames = multi.frame_block(rank, world, len(traj), args.steps)
+    warm = multi.frame_block(rank, world, len(traj), args.warmup)
+
+    # warm-up, then a cold cache for the timed block (frame 0 of the block decodes everything)
+    for f in warm:
+        r.render_into(traj[f], out_l, out_r, fmt, stream)
+    torch.cuda.synchronize()
+    r.reset_cache()
+    r.stats_history()
+
+    sampler = ClockSampler(local)
+    multi.barrier()
+    torch.cuda.synchronize()
+    sampler.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for f in frames:
+        r.render_into(traj[f], out_l, out_r, fmt, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    multi.barrier()
+    clocks = sampler.stop()
+    t_ms = e0.elapsed_time(e1)
+    t_max = multi.max_over_ranks(t_ms, dev)
+    hist = r.stats_history(max(args.steps, 1))
+    overflow = any(h["overflow"] for h in hist)
+
+    # end-to-end through the public API: host pose in, RGBA8 images into pinned host memory
+    r.reset_cache()
+    hl = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
+    hr = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
+    multi.barrier()
+    t0 = time.perf_counter()
+    for f in frames:
+        r.render_host(traj[f], hl, hr, fmt)
+    t1 = time.perf_counter()
+    multi.barrier()
+    e2e_max = multi.max_over_ranks(t1 - t0, dev)
+
+    total_frames = world * len(frames)
+    value = total_frames / (t_max / 1000.0) if t_max > 0 else 0.0
+
+    # per-stage measured ms (CUDA events inside the timed region) and roofline
+    stages = ["cull", "derive", "project", "depth_sort", "emit", "tile_sort", "ranges", "blend"]
+    ms = {s: sum(h["ms_" + s] for h in hist) for s in stages}
+    nf = max(1, len(hist))
+    algo = {s: 0.0 for s in stages}
+    for h in hist:
+        b = _stage_bytes(h, sc.n, 10, cfg.width, cfg.height, 4)
+        for s in stages:
+            algo[s] += b[s]
+    evals = sum(h["n_evals"] for h in hist)
+    peaks = _peaks()
+    dom = max(stages, key=lambda s: ms[s])
+    if dom == "blend":
+        # ALU bound: FP32 instructions of the per-(pixel, splat) evaluation
+        ops = evals * BLEND_OPS_PER_EVAL
+        peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12
+        achieved = ops / (ms[dom] / 1000.0) / 1e12
+        roof = {"kernel": "blend", "bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
+                "note": f"{BLEND_OPS_PER_EVAL} fp32 ops per evaluation x {evals / nf:.3g} evaluations/frame; "
+                        "peak = 148 SMs x 128 fp32 lanes x max SM clock"}
+    else:
+        achieved = algo[dom] / (ms[dom] / 1000.0) / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
+                "note": f"algorithmic bytes/frame {algo[dom] / nf:.4g}; peak {peaks['src']}"}
+    stage_report = {s: {"ms_per_frame": round(ms[s] / nf, 4),
+                        "GBps": round(algo[s] / (ms[s] / 1000.0) / 1e9, 1) if ms[s] > 0 else None}
+                    for s in stages}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, sc, traj, frames[:max(1, args.cpu_sample_frames)])
+
+    if rank == 0:
+        launches_per_frame = 14
+        line = {
+            "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": len(frames),
+            "warmup": args.warmup, "ms_per_step": round(t_max / max(1, len(frames)), 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (scenegen seed 7, SplitMix64)",
+            "config": {"workload": f"{args.config}: {sc.n}-anchor synthetic city, {cfg.width}x{cfg.height} "
+                                   f"binocular, {len(traj)}-frame ground-to-aerial trajectory, D_max {cfg.d_max}",
+                       "anchors": sc.n, "width": cfg.width, "height": cfg.height, "d_max": cfg.d_max,
+                       "frames_per_rank": len(frames), "out_format": "rgba8",
+                       "l2": "no flush: per-frame working set (pool/splat/pair traffic ~1-2 GB) > 126 MB L2",
+                       "parallelism": f"frames partitioned by view, scene replicated, dp{world}"},
+            "stages": stage_report,
+            "frame_counts": {"visible": round(sum(h["n_visible"] for h in hist) / nf),
+                             "misses": round(sum(h["n_misses"] for h in hist) / nf),
+                             "splats": round(sum(h["n_splats"] for h in hist) / nf),
+                             "pairs": round(sum(h["n_pairs"] for h in hist) / nf),
+                             "evals": round(evals / nf), "overflow": overflow},
+            "roofline": roof,
+            "e2e": {"value": round(total_frames / e2e_max, 3) if e2e_max > 0 else None, "unit": UNIT,
+                    "h2d_bytes_per_step": 120, "d2h_bytes_per_step": 2 * cfg.width * cfg.height * 4},
+            "gpu_launches": launches_per_frame * len(frames),
+            "clocks": clocks,
+        }
+        if cpu:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+
+
+BLEND_OPS_PER_EVAL = 11   # dx, dy, dx^2, dy^2, dx*dy, A*, C*, B*, +, *(-1/2), -  (minimum per evaluation)
+
+
+def cpu_baseline(cfg, sc, traj, frames):
+    """The oracle as it stands, on the host cores: full frames (state machine +
+    binocular raster) of the same trajectory from a cold cache."""
+    import oracle
+    oc = oracle.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max)
+    o = oracle.Oracle(sc, oc)
+    t0 = time.perf_counter()
+    for f in frames:
+        o.frame(traj[f])
+    dt = time.perf_counter() - t0
+    return {"value": round(len(frames) / dt, 5), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+            "sample": f"{len(frames)} full binocular frame(s) (frames {frames[0]}..{frames[-1]}, cold cache) of "
+                      f"the {cfg.name} trajectory: cull + derive + project + sort + blend, {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (CPU) on a bounded sample of the same workload."""
+    from paper_2502_14938_b200 import multi
+    rank, world, _ = multi.dist_env()
+    if rank != 0:
+        return
+    import scenegen as sg
+    import oracle
+    cfg = sg.config(args.config)
+    sc = cfg.scene()
+    traj = sg.trajectory(cfg)
+    oc = oracle.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max)
+    o = oracle.Oracle(sc, oc)
+    nref = max(1, min(args.steps, args.ref_frames))
+    frames = list(range(nref))
+    t0 = time.perf_counter()
+    for f in frames:
+        o.frame(traj[f])
+    dt = time.perf_counter() - t0
+    value = nref / dt
+    sample = (f"first {nref} consecutive frames of the {cfg.name} trajectory (cache state machine + full "
+              f"binocular raster per frame), {oracle.num_threads()} threads; the requested {args.steps} steps "
+              f"are bounded to {nref} to keep the run within minutes")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": round(value, 5), "unit": UNIT, "n_gpus": world,
+        "steps": nref, "requested_steps": args.steps, "warmup": 0, "ms_per_step": round(1000 * dt / nref, 1),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (scenegen seed 7, SplitMix64)",
+        "config": {"workload": f"{args.config} (same as the GPU arm)", "anchors": sc.n, "width": cfg.width,
+                   "height": cfg.height},
+        "cpu_baseline": {"value": round(value, 5), "unit": UNIT, "cores": oracle.num_threads(), "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=600)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="gsc", choices=["gsc", "reference"])
+    ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
+    ap.add_argument("--pair-capacity", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-frames", type=int, default=1)
+    ap.add_argument("--ref-frames", type=int, default=4)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_gsc(args)
+
+
+if __name__ == "__main__":
+    main()

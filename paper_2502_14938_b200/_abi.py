@@ -54,7 +54,8 @@ class gsc_frame_stats(C.Structure):
                 ("depth_next", C.c_int32), ("update_rate", C.c_float), ("novelty_rate", C.c_float),
                 ("ms_cull", C.c_float), ("ms_derive", C.c_float), ("ms_project", C.c_float),
                 ("ms_depth_sort", C.c_float), ("ms_emit", C.c_float), ("ms_tile_sort", C.c_float),
-                ("ms_ranges", C.c_float), ("ms_blend", C.c_float), ("ms_total", C.c_float)]
+                ("ms_ranges", C.c_float), ("ms_blend", C.c_float), ("ms_total", C.c_float),
+                ("n_evals", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

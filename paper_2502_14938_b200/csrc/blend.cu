@@ -21,7 +21,7 @@ constexpr int kBThreads = 256;
 __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
-             void *__restrict__ out_l, void *__restrict__ out_r, int fmt) {
+             void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
   __shared__ float4 sA[kBThreads];
   __shared__ float4 sB[kBThreads];
   __shared__ float sb[kBThreads];
@@ -36,6 +36,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int done = !inside;
+  uint32_t nev = 0;
   for (uint32_t b = rg.x; b < rg.y; b += kBThreads) {
     __syncthreads();
     uint32_t idx = b + t;
@@ -49,6 +50,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     const int cnt = min((uint32_t)kBThreads, rg.y - b);
     if (!done) {
       for (int k = 0; k < cnt; ++k) {
+        ++nev;
         const float4 a = sA[k];
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float4 q = sB[k];
@@ -69,6 +71,9 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     }
     if (__syncthreads_count(done) == kBThreads) break;
   }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
+  if ((t & 31) == 0 && nev) atomicAdd(&ctr->n_evals, (unsigned long long)nev);
   if (!inside) return;
   const float o0 = __fadd_rn(C0, __fmul_rn(T, fc.bg[0]));
   const float o1 = __fadd_rn(C1, __fmul_rn(T, fc.bg[1]));
@@ -90,8 +95,9 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
 }
 
 void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_vals, const float4 *spA,
-                  const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, cudaStream_t st) {
-  blend_kernel<<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt);
+                  const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, FrameCounters *ctr,
+                  cudaStream_t st) {
+  blend_kernel<<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
 }
 
 // elementary-function self test (parity sweeps through the C ABI)

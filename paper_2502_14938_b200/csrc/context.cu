@@ -36,7 +36,7 @@ void launch_emit(const EmitIn &, int, int, int, int, uint32_t, uint32_t *, uint3
                  int, cudaStream_t);
 void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const float4 *, const float4 *, const float4 *,
-                  void *, void *, int, cudaStream_t);
+                  void *, void *, int, FrameCounters *, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 int sort_tile_size();
 int emit_tile_size();
@@ -441,7 +441,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   launch_ranges(ctx->pkey_a.p, ctr, ctx->ranges.p, ctx->num_sms, st);
   mark();
   // a8
-  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, st);
+  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr, st);
   launch_record(ctr, ctx->rec_dev.p + slot_i, st);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
                      st));
@@ -465,17 +465,19 @@ static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
   s->n_splats = r.n_splat;
   s->n_pairs = r.n_pairs_raw;
   s->overflow = r.overflow;
+  s->n_evals = r.n_evals;
   s->depth_used = r.depth_used;
   s->depth_next = r.depth_next;
   s->update_rate = r.n_visible ? (float)r.n_miss / (float)r.n_visible : 0.0f;
   s->novelty_rate = r.n_visible ? (float)r.n_new / (float)r.n_visible : 0.0f;
   FrameSlot &slot = ctx->slots[slot_i];
   if (slot.timed && (ctx->cfg.flags & GSC_F_STAGE_TIMING)) {
-    float ms[kEvents - 1] = {0};
-    for (int k = 0; k + 1 < kEvents; ++k) cudaEventElapsedTime(&ms[k], slot.ev[k], slot.ev[k + 1]);
+    float ms[8] = {0};
+    for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], slot.ev[k], slot.ev[k + 1]);
     s->ms_cull = ms[0]; s->ms_derive = ms[1]; s->ms_project = ms[2]; s->ms_depth_sort = ms[3];
     s->ms_emit = ms[4]; s->ms_tile_sort = ms[5]; s->ms_ranges = ms[6]; s->ms_blend = ms[7];
     cudaEventElapsedTime(&s->ms_total, slot.ev[0], slot.ev[8]);
+    (void)cudaGetLastError();   // an event query must not leave a sticky error behind
   }
 }
 

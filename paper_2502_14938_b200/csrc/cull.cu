@@ -162,6 +162,7 @@ __global__ void record_kernel(const FrameCounters *ctr, FrameRecordDev *rec) {
   rec->n_splat = ctr->n_splat;
   rec->n_pairs_raw = ctr->n_pairs_raw;
   rec->overflow = ctr->overflow;
+  rec->n_evals = ctr->n_evals;
 }
 
 // load-time: m_i = max_j |O_ij (.) s_i|_2 + 3.33 max_k s_ik  (R8), packed with pos

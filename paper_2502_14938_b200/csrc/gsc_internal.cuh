@@ -42,6 +42,7 @@ struct FrameCounters {
   uint32_t n_pairs;            // min(raw, capacity)
   uint32_t overflow;
   uint32_t pad;
+  unsigned long long n_evals;  // blend: per-pixel splat evaluations
   uint32_t hist_depth[4][256];
   uint32_t hist_tile[2][256];
 };
@@ -80,6 +81,7 @@ struct EmitIn {
 struct FrameRecordDev {
   int32_t frame, depth_used, depth_next, pad0;
   uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, pad1, pad2;
+  unsigned long long n_evals;
 };
 
 // ---------------------------------------------------------------- helpers
