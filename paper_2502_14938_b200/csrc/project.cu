@@ -78,13 +78,28 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   float fy1 = fminf(floorf(__fmul_rn(__fadd_rn(o.v, ey), 0.0625f)), (float)(TH - 1));
   if (fx0 > fx1 || fy0 > fy1) return false;
   int tx0 = (int)fx0, tx1 = (int)fx1, ty0 = (int)fy0, ty1 = (int)fy1;
-  uint32_t n = 0;
-  for (int ty = ty0; ty <= ty1; ++ty)
-    for (int tx = tx0; tx <= tx1; ++tx) n += tile_kept(o.u, o.v, o.A, o.B, o.C, o.thr, tx, ty, width, height);
-  o.n = n;
+  o.n = 0;   // kept tiles: counted by the warp-flattened walk in the kernel
   o.box_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
   o.box_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
-  return n > 0;
+  return true;
+}
+
+// count the kept tiles of the 32 lanes' candidate boxes, balanced across the warp
+__device__ __forceinline__ uint32_t warp_count_kept(WarpTiles &ws, bool has, const SplatOut &o, int width,
+                                                    int height) {
+  TileJob j;
+  j.u = o.u; j.v = o.v; j.A = o.A; j.B = o.B; j.C = o.C; j.thr = o.thr;
+  j.tx0 = (int)(o.box_x & 0xFFFFu); j.ty0 = (int)(o.box_y & 0xFFFFu);
+  j.bw = (int)(o.box_x >> 16) - j.tx0 + 1; j.bh = (int)((o.box_y >> 16) & 0x7FFFu) - j.ty0 + 1;
+  const uint32_t total = warp_tiles_stage(ws, has, j, 0xFFFFFFFFu);
+  for (uint32_t w = lane_id(); w < total; w += 32) {
+    int owner, tx, ty;
+    if (warp_tiles_item(ws, w, width, height, owner, tx, ty)) atomicAdd(&ws.cnt[owner], 1u);
+  }
+  __syncwarp();
+  const uint32_t n = ws.cnt[lane_id()];
+  __syncwarp();
+  return has ? n : 0u;
 }
 
 __global__ void __launch_bounds__(kPThreads)
@@ -94,6 +109,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
   __shared__ uint32_t s_tile, s_prefix;
   __shared__ uint32_t s_cnt[2][kPItems][kPThreads / 32];
   __shared__ uint32_t s_hist[4][256];
+  __shared__ WarpTiles s_wt[kPThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
   const uint32_t S = ctr->n_visible * (uint32_t)kK;
@@ -139,6 +155,10 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int it = 0; it < kPItems; ++it) {
+        if (__any_sync(0xFFFFFFFFu, ok[it][e])) {
+          so[it][e].n = warp_count_kept(s_wt[warp], ok[it][e], so[it][e], fc.width, fc.height);
+          ok[it][e] = ok[it][e] && so[it][e].n > 0;
+        }
         m[e][it] = __ballot_sync(0xFFFFFFFFu, ok[it][e]);
         if (lane == 0) s_cnt[e][it][warp] = __popc(m[e][it]);
         if (ok[it][e]) pairs_local += so[it][e].n;

@@ -177,32 +177,31 @@ emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint
             uint32_t *__restrict__ vals_out, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_tile, s_prefix, s_w[kEThreads / 32];
   __shared__ uint32_t s_hist[2][256];
-  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id();
+  __shared__ WarpTiles s_wt[kEThreads / 32];
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id(), lt = lanemask_lt();
   for (int k = t; k < 512; k += kEThreads) (&s_hist[0][0])[k] = 0;
   const uint32_t C = ctr->n_splat;
   const uint32_t ntiles = (C + kETile - 1) / kETile;
+  WarpTiles &ws = s_wt[warp];
   for (;;) {
     __syncthreads();
     if (t == 0) s_tile = atomicAdd(&ctr->tile_emit, 1u);
     __syncthreads();
     const uint32_t tile = s_tile;
     if (tile >= ntiles) break;
-    const uint32_t p0 = tile * kETile + t * kEItems;
+    // warp-striped: round i, lane l -> sorted position tile*1024 + warp*128 + i*32 + l
+    const uint32_t p0 = tile * kETile + warp * (32 * kEItems) + lane;
     uint32_t c[kEItems], cnt[kEItems], sum = 0;
 #pragma unroll
     for (int i = 0; i < kEItems; ++i) {
-      uint32_t p = p0 + i;
+      uint32_t p = p0 + 32 * i;
       c[i] = p < C ? in.sorted[p] : 0u;
       cnt[i] = p < C ? in.count[c[i]] : 0u;
       sum += cnt[i];
     }
-    uint32_t inc = sum;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t v = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-      if (lane >= (uint32_t)o) inc += v;
-    }
-    if (lane == 31) s_w[warp] = inc;
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
+    if (lane == 0) s_w[warp] = sum;
     __syncthreads();
     if (warp == 0) {
       uint32_t wv = lane < kEThreads / 32 ? s_w[lane] : 0u, wi = wv;
@@ -231,29 +230,45 @@ emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint
       }
     }
     __syncthreads();
-    uint32_t off = s_prefix + s_w[warp] + inc - sum;
-#pragma unroll
+    uint32_t run = s_prefix + s_w[warp];
+#pragma unroll 1
     for (int i = 0; i < kEItems; ++i) {
-      if (cnt[i] == 0) continue;
-      const uint32_t ci = c[i];
-      const float4 a = in.spA[ci];
-      const float Cc = in.spB[ci].x;
-      const float thr = in.spC[ci].y;
-      const uint2 bx = in.box[ci];
-      const int tx0 = bx.x & 0xFFFF, tx1 = bx.x >> 16, ty0 = bx.y & 0xFFFF, ty1 = (bx.y >> 16) & 0x7FFF;
-      const uint32_t ebase = (bx.y >> 31) ? (uint32_t)Te : 0u;
-      for (int ty = ty0; ty <= ty1; ++ty)
-        for (int tx = tx0; tx <= tx1; ++tx)
-          if (tile_kept(a.x, a.y, a.z, a.w, Cc, thr, tx, ty, width, height)) {
-            uint32_t key = ebase + (uint32_t)(ty * TW + tx);
-            if (off < cap) {
-              keys_out[off] = key;
-              vals_out[off] = ci;
-              atomicAdd(&s_hist[0][key & 0xFFu], 1u);
-              atomicAdd(&s_hist[1][(key >> 8) & 0xFFu], 1u);
-            }
-            ++off;
-          }
+      const bool has = cnt[i] > 0;
+      if (!__any_sync(0xFFFFFFFFu, has)) continue;
+      TileJob j{};
+      uint32_t kb = 0;
+      if (has) {
+        const uint32_t ci = c[i];
+        const float4 a = in.spA[ci];
+        const uint2 bx = in.box[ci];
+        j.u = a.x; j.v = a.y; j.A = a.z; j.B = a.w; j.C = in.spB[ci].x; j.thr = in.spC[ci].y;
+        j.tx0 = (int)(bx.x & 0xFFFFu); j.ty0 = (int)(bx.y & 0xFFFFu);
+        j.bw = (int)(bx.x >> 16) - j.tx0 + 1; j.bh = (int)((bx.y >> 16) & 0x7FFFu) - j.ty0 + 1;
+        kb = (bx.y >> 31) ? (uint32_t)Te : 0u;
+      }
+      ws.id[lane] = c[i];
+      ws.kb[lane] = kb;
+      const uint32_t total = warp_tiles_stage(ws, has, j, cnt[i]);
+      for (uint32_t w0 = 0; w0 < total; w0 += 32) {
+        const uint32_t w = w0 + lane;
+        int owner = 0, tx = 0, ty = 0;
+        const bool kept = w < total && warp_tiles_item(ws, w, width, height, owner, tx, ty);
+        const uint32_t mask = __ballot_sync(0xFFFFFFFFu, kept);
+        const uint32_t pos = run + __popc(mask & lt);
+        const uint32_t key = kept ? ws.kb[owner] + (uint32_t)(ty * TW + tx) : 0xFFFFFFFFu;
+        const bool wr = kept && pos < cap;
+        if (wr) {
+          keys_out[pos] = key;
+          vals_out[pos] = ws.id[owner];
+          atomicAdd(&s_hist[0][key & 0xFFu], 1u);
+        }
+        // high digit: mostly shared inside a warp step -> aggregate with match_any
+        const uint32_t hi = wr ? (key >> 8) & 0xFFu : 0x100u;
+        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, hi);
+        if (wr && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[1][hi], (uint32_t)__popc(peers));
+        run += __popc(mask);
+      }
+      __syncwarp();
     }
   }
   __syncthreads();
