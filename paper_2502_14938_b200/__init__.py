@@ -139,7 +139,7 @@ class Renderer:
         if what == "pool":
             out = out.reshape(-1, 13)
         elif what == "splats":
-            out = out.reshape(-1, 12)
+            out = out.reshape(-1, 13)
         elif what == "ranges":
             out = out.reshape(-1, 2)
         return out

@@ -652,19 +652,21 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       return GSC_OK;
     }
     case GSC_DBG_SPLATS: {
-      *len = ns * 12 * 4;
+      *len = ns * 13 * 4;
       if (!host_dst || !cap) return GSC_OK;
       std::vector<float4> A(ns), B(ns), Cc(ns);
       std::vector<uint2> bx(ns);
+      std::vector<uint32_t> cn(ns);
       CU(cudaMemcpy(A.data(), ctx->spA.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(B.data(), ctx->spB.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(Cc.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(bx.data(), ctx->box.p, ns * 8, cudaMemcpyDeviceToHost));
-      std::vector<float> out(ns * 12);
+      CU(cudaMemcpy(cn.data(), ctx->count.p, ns * 4, cudaMemcpyDeviceToHost));
+      std::vector<float> out(ns * 13);
       for (size_t k = 0; k < ns; ++k) {
-        float r[12] = {A[k].x, A[k].y, A[k].z, A[k].w, B[k].x, B[k].y, B[k].z, B[k].w, Cc[k].x, Cc[k].z, Cc[k].y,
-                       (float)(bx[k].y >> 31)};
-        std::memcpy(&out[12 * k], r, sizeof(r));
+        float r[13] = {A[k].x, A[k].y, A[k].z, A[k].w, B[k].x, B[k].y, B[k].z, B[k].w, Cc[k].x, Cc[k].z, Cc[k].y,
+                       (float)(bx[k].y >> 31), (float)cn[k]};
+        std::memcpy(&out[13 * k], r, sizeof(r));
       }
       std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));
       return GSC_OK;

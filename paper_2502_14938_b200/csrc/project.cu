@@ -4,20 +4,22 @@
 // tile-coverage count (FlashGS citation), both eyes batched
 // ("independently or in batching"; R19).
 //
-// One thread per visible slot s = v*K + j (Gaussian g = X_f[v]*K + j),
-// 2 slots per thread, 512 slots per tile.  A dead slot costs its 4-byte alpha
-// read; a live one adds its 48-byte pool record.  Splats with >= 1 kept tile
-// are compacted in (eye, s) order -- the order that makes the later stable
-// sorts break depth ties by g like the oracle -- with a decoupled look-back.
-// Also fused: the 4 x 256-bin digit histogram of the depth keys (first pass
-// of the onesweep depth sort) and the pair count.
+// Warp-centric and barrier-free: each warp acquires its own tile of 64 visible
+// slots s = v*K + j (Gaussian g = X_f[v]*K + j), 2 per lane.  A dead slot
+// costs its 4-byte alpha read; a live one adds its 48-byte pool record.
+// Splats whose candidate tile box is non-empty are compacted in (eye, s)
+// order -- the order that makes the later stable sorts break depth ties by g
+// like the oracle -- with a warp-level decoupled look-back whose aggregate is
+// published BEFORE the expensive kept-tile count, so a warp holding a huge
+// splat never stalls its successors.  Fused: the 4 x 256-bin digit histogram
+// of the depth keys (first pass of the onesweep depth sort) and the pair count.
 #include "gsc_internal.cuh"
 
 namespace gsc {
 
 constexpr int kPThreads = 256;
 constexpr int kPItems = 2;
-constexpr int kPTile = kPThreads * kPItems;
+constexpr int kPTile = 32 * kPItems;   // slots per warp tile
 
 struct SplatOut {
   float u, v, A, B, C, thr;
@@ -78,7 +80,7 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   float fy1 = fminf(floorf(__fmul_rn(__fadd_rn(o.v, ey), 0.0625f)), (float)(TH - 1));
   if (fx0 > fx1 || fy0 > fy1) return false;
   int tx0 = (int)fx0, tx1 = (int)fx1, ty0 = (int)fy0, ty1 = (int)fy1;
-  o.n = 0;   // kept tiles: counted by the warp-flattened walk in the kernel
+  o.n = 0;   // kept tiles: counted by the warp-flattened walk
   o.box_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
   o.box_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
   return true;
@@ -106,31 +108,30 @@ __global__ void __launch_bounds__(kPThreads)
 project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__restrict__ alpha,
                const float4 *__restrict__ pool, SplatBufs sb, uint32_t *__restrict__ status,
                FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_tile, s_prefix;
-  __shared__ uint32_t s_cnt[2][kPItems][kPThreads / 32];
   __shared__ uint32_t s_hist[4][256];
   __shared__ WarpTiles s_wt[kPThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
   const uint32_t S = ctr->n_visible * (uint32_t)kK;
   const uint32_t ntiles = (S + kPTile - 1) / kPTile;
+  WarpTiles &ws = s_wt[warp];
   uint32_t pairs_local = 0;
 
   for (;;) {
-    __syncthreads();
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_project, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(&ctr->tile_project, 1u);
+    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
     if (tile >= ntiles) break;
 
     SplatOut so[kPItems][2];
     bool ok[kPItems][2];
     uint32_t gs[kPItems];
-    float4 q0[kPItems], q1[kPItems], q2[kPItems];
+    float4 q2[kPItems];
     float al[kPItems];
 #pragma unroll
     for (int it = 0; it < kPItems; ++it) {
-      uint32_t s = tile * kPTile + it * kPThreads + warp * 32 + lane;
+      const uint32_t s = tile * kPTile + it * 32 + lane;
       ok[it][0] = ok[it][1] = false;
       al[it] = 0.0f;
       gs[it] = 0;
@@ -140,82 +141,70 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
         gs[it] = g;
         al[it] = alpha[g];
         if (__fmul_rn(255.0f, al[it]) > 1.0f) {
-          q0[it] = pool[3 * (size_t)g];
-          q1[it] = pool[3 * (size_t)g + 1];
+          const float4 q0 = pool[3 * (size_t)g];
+          const float4 q1 = pool[3 * (size_t)g + 1];
           q2[it] = pool[3 * (size_t)g + 2];
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0[it], q1[it], q2[it],
-                                    so[it][e]);
+            ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0, q1, q2[it], so[it][e]);
         }
       }
     }
-    uint32_t m[2][kPItems];
+    // compaction masks in (eye, item, lane) order; publish the aggregate early
+    uint32_t m[2][kPItems], agg = 0;
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int it = 0; it < kPItems; ++it) {
-        if (__any_sync(0xFFFFFFFFu, ok[it][e])) {
-          so[it][e].n = warp_count_kept(s_wt[warp], ok[it][e], so[it][e], fc.width, fc.height);
-          ok[it][e] = ok[it][e] && so[it][e].n > 0;
-        }
         m[e][it] = __ballot_sync(0xFFFFFFFFu, ok[it][e]);
-        if (lane == 0) s_cnt[e][it][warp] = __popc(m[e][it]);
-        if (ok[it][e]) pairs_local += so[it][e].n;
+        agg += __popc(m[e][it]);
       }
-    __syncthreads();
-    if (warp == 0) {
-      // exclusive scan over the 2 * kPItems * 8 = 32 counts in (eye, item, warp) order
-      uint32_t c = (&s_cnt[0][0][0])[lane];
-      uint32_t inc = c;
+    if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
+    // kept-tile counts (the expensive part) while predecessors publish
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t tv = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-        if (lane >= (uint32_t)o) inc += tv;
-      }
-      uint32_t agg = __shfl_sync(0xFFFFFFFFu, inc, 31);
-      (&s_cnt[0][0][0])[lane] = inc - c;
-      uint32_t pre = 0;
-      if (tile == 0) {
-        if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
-      } else {
-        if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
-        pre = lookback_u32(status, tile);
-        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-      }
-      if (lane == 0) {
-        s_prefix = pre;
-        if (tile == ntiles - 1) ctr->n_splat = pre + agg;
-      }
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int it = 0; it < kPItems; ++it)
+        if (m[e][it]) {
+          so[it][e].n = warp_count_kept(ws, ok[it][e], so[it][e], fc.width, fc.height);
+          if (ok[it][e]) pairs_local += so[it][e].n;
+        }
+    uint32_t pre = 0;
+    if (tile > 0) {
+      pre = lookback_u32(status, tile);
+      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
     }
-    __syncthreads();
+    if (lane == 0 && tile == ntiles - 1) ctr->n_splat = pre + agg;
+    uint32_t base = pre;
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int it = 0; it < kPItems; ++it) {
-        if (!ok[it][e]) continue;
-        const SplatOut &o = so[it][e];
-        uint32_t c = s_prefix + s_cnt[e][it][warp] + __popc(m[e][it] & lt);
-        sb.spA[c] = make_float4(o.u, o.v, o.A, o.B);
-        sb.spB[c] = make_float4(o.C, al[it], q2[it].y, q2[it].z);
-        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-        sb.count[c] = o.n;
-        uint32_t dk = __float_as_uint(o.depth);
-        sb.spC[c] = make_float4(q2[it].w, o.thr, __uint_as_float(dk), 0.0f);
-        sb.depth[c] = dk;
-        sb.gslot[c] = gs[it];
+        if (ok[it][e]) {
+          const SplatOut &o = so[it][e];
+          const uint32_t c = base + __popc(m[e][it] & lt);
+          sb.spA[c] = make_float4(o.u, o.v, o.A, o.B);
+          sb.spB[c] = make_float4(o.C, al[it], q2[it].y, q2[it].z);
+          sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
+          sb.count[c] = o.n;
+          const uint32_t dk = __float_as_uint(o.depth);
+          sb.spC[c] = make_float4(q2[it].w, o.thr, __uint_as_float(dk), 0.0f);
+          sb.depth[c] = dk;
+          sb.gslot[c] = gs[it];
 #pragma unroll
-        for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
+          for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
+        }
+        base += __popc(m[e][it]);
       }
   }
   // flush the fused histogram and the pair count
+  for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
+  if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
   __syncthreads();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) {
     uint32_t v = (&s_hist[0][0])[k];
     if (v) atomicAdd(&ctr->hist_depth[0][0] + k, v);
   }
-  for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
-  if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
 }
 
 static int g_project_grid = 0;

@@ -170,27 +170,28 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
 // project is re-evaluated to enumerate the kept tiles (identical arithmetic).
 constexpr int kEThreads = 256;
 constexpr int kEItems = 4;
-constexpr int kETile = kEThreads * kEItems;
+constexpr int kETile = 32 * kEItems;   // sorted positions per warp tile
 
+// Warp-centric and barrier-free: a warp acquires a tile of 128 sorted
+// positions, publishes its pair count, looks back, then walks its rounds.
 __global__ void __launch_bounds__(kEThreads)
 emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint32_t *__restrict__ keys_out,
             uint32_t *__restrict__ vals_out, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_tile, s_prefix, s_w[kEThreads / 32];
   __shared__ uint32_t s_hist[2][256];
   __shared__ WarpTiles s_wt[kEThreads / 32];
   const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id(), lt = lanemask_lt();
   for (int k = t; k < 512; k += kEThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
   const uint32_t C = ctr->n_splat;
   const uint32_t ntiles = (C + kETile - 1) / kETile;
   WarpTiles &ws = s_wt[warp];
   for (;;) {
-    __syncthreads();
-    if (t == 0) s_tile = atomicAdd(&ctr->tile_emit, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(&ctr->tile_emit, 1u);
+    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
     if (tile >= ntiles) break;
-    // warp-striped: round i, lane l -> sorted position tile*1024 + warp*128 + i*32 + l
-    const uint32_t p0 = tile * kETile + warp * (32 * kEItems) + lane;
+    // round i, lane l -> sorted position tile*128 + i*32 + l
+    const uint32_t p0 = tile * kETile + lane;
     uint32_t c[kEItems], cnt[kEItems], sum = 0;
 #pragma unroll
     for (int i = 0; i < kEItems; ++i) {
@@ -201,37 +202,22 @@ emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-    if (lane == 0) s_w[warp] = sum;
-    __syncthreads();
-    if (warp == 0) {
-      uint32_t wv = lane < kEThreads / 32 ? s_w[lane] : 0u, wi = wv;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        uint32_t v = __shfl_up_sync(0xFFFFFFFFu, wi, o);
-        if (lane >= (uint32_t)o) wi += v;
-      }
-      uint32_t agg = __shfl_sync(0xFFFFFFFFu, wi, 31);
-      if (lane < kEThreads / 32) s_w[lane] = wi - wv;
-      uint32_t pre = 0;
-      if (tile == 0) {
-        if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
-      } else {
-        if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
-        pre = lookback_u32(status, tile);
-        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-      }
-      if (lane == 0) {
-        s_prefix = pre;
-        if (tile == ntiles - 1) {
-          uint32_t tot = pre + agg;
-          ctr->n_pairs = tot < cap ? tot : cap;
-          ctr->overflow = tot > cap;
-        }
-      }
+    const uint32_t agg = sum;
+    uint32_t pre = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
+    } else {
+      if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
+      pre = lookback_u32(status, tile);
+      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
     }
-    __syncthreads();
-    uint32_t run = s_prefix + s_w[warp];
-#pragma unroll 1
+    if (lane == 0 && tile == ntiles - 1) {
+      const uint32_t tot = pre + agg;
+      ctr->n_pairs = tot < cap ? tot : cap;
+      ctr->overflow = tot > cap;
+    }
+    uint32_t run = pre;
+#pragma unroll
     for (int i = 0; i < kEItems; ++i) {
       const bool has = cnt[i] > 0;
       if (!__any_sync(0xFFFFFFFFu, has)) continue;

@@ -56,10 +56,11 @@ def compare_splats_pairs(o, r):
         og, orec = o.splats(e)
         keep = orec[:, 11] > 0
         og, orec = og[keep], orec[keep]
-        m = eye == e
+        m = (eye == e) & (sp[:, 12] > 0)          # splats with >= 1 kept tile
         assert np.array_equal(sg[m], og), f"splat set of eye {e} differs ({m.sum()} vs {len(og)})"
-        # u v A B C alpha r g b depth thr
+        # u v A B C alpha r g b depth thr, and the kept-tile count
         assert np.array_equal(sp[m][:, :11], orec[:, :11]), f"splat records of eye {e} differ"
+        assert np.array_equal(sp[m][:, 12], orec[:, 11]), f"kept-tile counts of eye {e} differ"
     ok, og = o.pairs()
     gk, gg = r.debug("pairs"), r.debug("pair_g")
     assert len(gk) == len(ok), f"pair counts differ ({len(gk)} vs {len(ok)})"
