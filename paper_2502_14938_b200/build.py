@@ -13,7 +13,7 @@ OBJ = os.path.join(HERE, "build_obj")
 SO = os.path.join(HERE, "libgscache.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["cull.cu", "derive.cu", "project.cu", "sort.cu", "blend.cu", "context.cu"]
+SOURCES = ["cull.cu", "derive.cu", "project.cu", "sort.cu", "emit.cu", "blend.cu", "context.cu"]
 HEADERS = ["gsc_internal.cuh"]
 
 # -fmad=false / -prec-* / -ftz=false: fp32 ops are emitted exactly as written

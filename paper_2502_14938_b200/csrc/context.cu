@@ -32,8 +32,7 @@ void launch_project(const FrameC &, const uint32_t *, const float *, const float
 int project_tile_size();
 void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, const uint32_t *,
                      uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
-void launch_emit(const EmitIn &, int, int, int, int, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *,
-                 int, cudaStream_t);
+void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, cudaStream_t);
 void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const float4 *, const float4 *, const float4 *,
                   void *, void *, int, FrameCounters *, cudaStream_t);
@@ -97,7 +96,7 @@ struct gsc_ctx {
   size_t cap_splat = 0, cap_pairs = 0;
   DevBuf<float4> spA, spB, spC;
   DevBuf<uint2> box;
-  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot;
+  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list;
   DevBuf<uint32_t> pkey_a, pval_a, pkey_b, pval_b;
   DevBuf<uint2> ranges;
   DevBuf<uint32_t> sort_status_a, sort_status_b;
@@ -307,6 +306,9 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   int64_t pc = ctx->cfg.pair_capacity > 0 ? ctx->cfg.pair_capacity : std::max<int64_t>(1 << 24, 4 * (int64_t)NK);
   pc = std::min<int64_t>(pc, (1LL << 30) - 1);
   ctx->cap_pairs = (size_t)pc;
+  CU(ctx->list_off.alloc(ctx->cap_splat));
+  CU(ctx->pair_off.alloc(ctx->cap_splat));
+  CU(ctx->list.alloc(std::min<size_t>(2 * ctx->cap_pairs, (1u << 31) - 1)));
   CU(ctx->pkey_a.alloc(ctx->cap_pairs));
   CU(ctx->pval_a.alloc(ctx->cap_pairs));
   CU(ctx->pkey_b.alloc(ctx->cap_pairs));
@@ -419,7 +421,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
                 ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, st);
   mark();
   // a4
-  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p};
+  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
+               ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
   launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, sb,
                  reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
   mark();
@@ -428,8 +431,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
                   &ctr->hist_depth[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[0],
                   ctx->num_sms, st);
   mark();
-  EmitIn ei{ctx->dval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p};
-  launch_emit(ei, fc.width, fc.height, fc.TW, fc.Te, (uint32_t)ctx->cap_pairs, ctx->pkey_a.p, ctx->pval_a.p,
+  EmitIn ei{ctx->dval_a.p, ctx->count.p, ctx->list_off.p, ctx->list.p, ctx->pair_off.p};
+  launch_emit(ei, (uint32_t)ctx->cap_pairs, ctx->pkey_a.p, ctx->pval_a.p,
               reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_emit), ctr, ctx->num_sms, st);
   mark();
   // a6 (tile digits)

@@ -1,0 +1,165 @@
+// emit.cu -- SURVEY §8(a) rows a5 (tile-key duplication) and a7 (tile ranges).
+//
+// Duplication happens between the depth digits and the tile digits of the
+// (tile, depth) LSD radix sort (sort.cu): the splats arrive stably sorted by
+// depth, and every splat's kept tiles (keys written by project.cu into the
+// kept-tile list, row-major) are expanded into (tile key, splat) pairs in that
+// order ("key-value pairs").
+//
+//   pairoff: exclusive scan of the kept-tile counts in depth order
+//            (warp-level decoupled look-back) -> pair_off[p], P
+//   expand : load-balanced expansion -- each warp owns 256 consecutive OUTPUT
+//            positions q and finds the owning splat by a 32-ary cooperative
+//            search of pair_off, so the heavy-tailed splat sizes (near splats
+//            are both the biggest and the first in depth order) cost nothing
+//            extra; reads of the list are contiguous runs, writes coalesced.
+//            Fused: the 2 x 256-bin digit histogram of the tile keys.
+//   ranges : [start, end) per (eye, tile) from the tile-sorted keys.
+#include "gsc_internal.cuh"
+
+namespace gsc {
+
+constexpr int kXThreads = 256;
+constexpr int kOffItems = 8;
+constexpr int kOffTile = 32 * kOffItems;   // sorted positions per warp tile
+constexpr int kExpItems = 8;
+constexpr int kExpChunk = 32 * kExpItems;  // output positions per warp chunk
+
+__global__ void __launch_bounds__(kXThreads)
+pairoff_kernel(EmitIn in, uint32_t cap, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  const uint32_t C = ctr->n_splat;
+  const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
+  for (;;) {
+    uint32_t tile = 0;
+    if (lane == 0) tile = atomicAdd(&ctr->tile_pairoff, 1u);
+    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
+    if (tile >= ntiles) break;
+    uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
+#pragma unroll
+    for (int i = 0; i < kOffItems; ++i) {
+      const uint32_t p = tile * kOffTile + i * 32 + lane;
+      cnt[i] = p < C ? in.count[in.sorted[p]] : 0u;
+    }
+#pragma unroll
+    for (int i = 0; i < kOffItems; ++i) {
+      uint32_t inc = cnt[i];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        if (lane >= (uint32_t)o) inc += t;
+      }
+      excl[i] = run + inc - cnt[i];
+      run += __shfl_sync(0xFFFFFFFFu, inc, 31);
+    }
+    const uint32_t agg = run;
+    uint32_t pre = 0;
+    if (tile == 0) {
+      if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
+    } else {
+      if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
+      pre = lookback_u32(status, tile);
+      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+    }
+#pragma unroll
+    for (int i = 0; i < kOffItems; ++i) {
+      const uint32_t p = tile * kOffTile + i * 32 + lane;
+      if (p < C) in.pair_off[p] = pre + excl[i];
+    }
+    if (lane == 0 && tile == ntiles - 1) {
+      const uint32_t tot = pre + agg;
+      ctr->n_pairs = tot < cap ? tot : cap;
+      if (tot > cap) ctr->overflow = 1u;
+    }
+    (void)lt;
+  }
+}
+
+// largest p in [0, C) with pair_off[p] <= q (pair_off[0] = 0 <= q), whole warp
+__device__ __forceinline__ uint32_t warp_find(const uint32_t *__restrict__ pair_off, uint32_t C, uint32_t q) {
+  const uint32_t lane = lane_id();
+  uint32_t lo = 0, hi = C - 1;
+  while (hi - lo >= 32) {
+    const uint32_t step = (hi - lo + 31) / 32;
+    const uint32_t idx = min(lo + lane * step, hi);
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, pair_off[idx] <= q);
+    const uint32_t l = 31 - __clz(mask);
+    const uint32_t nlo = min(lo + l * step, hi);
+    if (l < 31) hi = min(hi, lo + (l + 1) * step - 1);
+    lo = nlo;
+  }
+  const uint32_t idx = lo + lane;
+  const bool ok = idx <= hi && pair_off[idx] <= q;
+  const uint32_t mask = __ballot_sync(0xFFFFFFFFu, ok);
+  return lo + (31 - __clz(mask));
+}
+
+__global__ void __launch_bounds__(kXThreads)
+expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+              FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_hist[2][256];
+  for (int k = threadIdx.x; k < 512; k += kXThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t lane = lane_id();
+  const uint32_t P = ctr->n_pairs, C = ctr->n_splat;
+  const uint32_t nchunks = (P + kExpChunk - 1) / kExpChunk;
+  const uint32_t gw = (blockIdx.x * kXThreads + threadIdx.x) >> 5, nw = (gridDim.x * kXThreads) >> 5;
+  for (uint32_t ch = gw; ch < nchunks; ch += nw) {
+    const uint32_t q0 = ch * kExpChunk, q1 = min(q0 + kExpChunk, P) - 1;
+    const uint32_t pa = warp_find(in.pair_off, C, q0), pb = warp_find(in.pair_off, C, q1);
+#pragma unroll
+    for (int i = 0; i < kExpItems; ++i) {
+      const uint32_t q = q0 + i * 32 + lane;
+      if (q > q1) break;
+      uint32_t lo = pa, hi = pb;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (in.pair_off[mid] <= q) lo = mid; else hi = mid - 1;
+      }
+      const uint32_t c = in.sorted[lo];
+      const uint32_t key = in.list[in.list_off[c] + (q - in.pair_off[lo])];
+      keys_out[q] = key;
+      vals_out[q] = c;
+      atomicAdd(&s_hist[0][key & 0xFFu], 1u);
+      atomicAdd(&s_hist[1][(key >> 8) & 0xFFu], 1u);
+    }
+  }
+  __syncthreads();
+  for (int k = threadIdx.x; k < 512; k += kXThreads) {
+    const uint32_t v = (&s_hist[0][0])[k];
+    if (v) atomicAdd(&ctr->hist_tile[0][0] + k, v);
+  }
+}
+
+__global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *__restrict__ ctr,
+                              uint2 *__restrict__ ranges) {
+  const uint32_t P = ctr->n_pairs;
+  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
+    const uint32_t k = keys[p];
+    if (p == 0 || keys[p - 1] != k) ranges[k].x = p;
+    if (p == P - 1 || keys[p + 1] != k) ranges[k].y = p + 1;
+  }
+}
+
+static int g_off_grid = 0, g_exp_grid = 0;
+
+void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *vals_out, uint32_t *status,
+                 FrameCounters *ctr, int num_sms, cudaStream_t st) {
+  if (!g_off_grid) {
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_kernel, kXThreads, 0);
+    g_off_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_kernel, kXThreads, 0);
+    g_exp_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  }
+  pairoff_kernel<<<g_off_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
+  expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr);
+}
+
+void launch_ranges(const uint32_t *keys, const FrameCounters *ctr, uint2 *ranges, int num_sms, cudaStream_t st) {
+  ranges_kernel<<<num_sms * 4, 256, 0, st>>>(keys, ctr, ranges);
+}
+
+int emit_tile_size() { return kOffTile; }
+
+}  // namespace gsc

@@ -41,8 +41,9 @@ struct FrameCounters {
   uint32_t n_pairs_raw;        // pairs the frame needed
   uint32_t n_pairs;            // min(raw, capacity)
   uint32_t overflow;
-  uint32_t pad;
+  uint32_t list_top;           // project: bump allocator of the kept-tile list
   unsigned long long n_evals;  // blend: per-pixel splat evaluations
+  uint32_t tile_pairoff, tile_expand, pad2[2];
   uint32_t hist_depth[4][256];
   uint32_t hist_tile[2][256];
 };
@@ -66,15 +67,17 @@ struct SplatBufs {
   uint32_t *count;   // kept tiles
   uint32_t *depth;   // depth key = bits(z) (depth-sort input)
   uint32_t *gslot;   // Gaussian slot g
+  uint32_t *list_off;  // start of the splat's kept-tile keys in `list`
+  uint32_t *list;      // kept-tile keys (eye*T_e + ty*TW + tx), per splat contiguous, row-major
+  uint32_t list_cap;
 };
 
 struct EmitIn {
-  const uint32_t *sorted;   // splat indices in depth order
-  const float4 *spA;
-  const float4 *spB;
-  const float4 *spC;
-  const uint2 *box;
-  const uint32_t *count;
+  const uint32_t *sorted;    // splat indices in depth order
+  const uint32_t *count;     // kept tiles per splat
+  const uint32_t *list_off;
+  const uint32_t *list;
+  uint32_t *pair_off;        // exclusive scan of count in depth order
 };
 
 // snapshot copied to host every frame

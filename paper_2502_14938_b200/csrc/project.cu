@@ -86,22 +86,49 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   return true;
 }
 
-// count the kept tiles of the 32 lanes' candidate boxes, balanced across the warp
-__device__ __forceinline__ uint32_t warp_count_kept(WarpTiles &ws, bool has, const SplatOut &o, int width,
-                                                    int height) {
+// Test the 32 lanes' candidate boxes (balanced walk), count the kept tiles per
+// lane and append their keys to the kept-tile list: the warp bump-allocates
+// `total` slots (an upper bound), kept keys are written contiguously in walk
+// order, so lane l's keys start at base + sum of the kept counts of lanes < l.
+__device__ __forceinline__ uint32_t warp_count_list(WarpTiles &ws, bool has, const SplatOut &o, uint32_t kb,
+                                                    int width, int height, int TW, uint32_t *list, uint32_t list_cap,
+                                                    uint32_t *list_top, uint32_t *overflow, uint32_t &list_off) {
   TileJob j;
   j.u = o.u; j.v = o.v; j.A = o.A; j.B = o.B; j.C = o.C; j.thr = o.thr;
   j.tx0 = (int)(o.box_x & 0xFFFFu); j.ty0 = (int)(o.box_y & 0xFFFFu);
   j.bw = (int)(o.box_x >> 16) - j.tx0 + 1; j.bh = (int)((o.box_y >> 16) & 0x7FFFu) - j.ty0 + 1;
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
   const uint32_t total = warp_tiles_stage(ws, has, j, 0xFFFFFFFFu);
-  for (uint32_t w = lane_id(); w < total; w += 32) {
-    int owner, tx, ty;
-    if (warp_tiles_item(ws, w, width, height, owner, tx, ty)) atomicAdd(&ws.cnt[owner], 1u);
+  uint32_t base = 0;
+  if (lane == 0) {
+    base = atomicAdd(list_top, total);
+    if (base + total > list_cap || base + total < base) atomicExch(overflow, 1u);
+  }
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  uint32_t run = base;
+  for (uint32_t w0 = 0; w0 < total; w0 += 32) {
+    const uint32_t w = w0 + lane;
+    int owner = 0, tx = 0, ty = 0;
+    const bool kept = w < total && warp_tiles_item(ws, w, width, height, owner, tx, ty);
+    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, kept);
+    if (kept) {
+      atomicAdd(&ws.cnt[owner], 1u);
+      const uint32_t pos = run + __popc(mask & lt);
+      if (pos < list_cap) list[pos] = kb + (uint32_t)(ty * TW + tx);
+    }
+    run += __popc(mask);
   }
   __syncwarp();
-  const uint32_t n = ws.cnt[lane_id()];
+  const uint32_t n = has ? ws.cnt[lane] : 0u;
   __syncwarp();
-  return has ? n : 0u;
+  uint32_t inc = n;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+    if (lane >= (uint32_t)off) inc += t;
+  }
+  list_off = base + inc - n;
+  return n;
 }
 
 __global__ void __launch_bounds__(kPThreads)
@@ -160,13 +187,15 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
         agg += __popc(m[e][it]);
       }
     if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-    // kept-tile counts (the expensive part) while predecessors publish
+    // kept-tile counts and lists (the expensive part) while predecessors publish
+    uint32_t loff[kPItems][2];
 #pragma unroll
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int it = 0; it < kPItems; ++it)
         if (m[e][it]) {
-          so[it][e].n = warp_count_kept(ws, ok[it][e], so[it][e], fc.width, fc.height);
+          so[it][e].n = warp_count_list(ws, ok[it][e], so[it][e], e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
+                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff[it][e]);
           if (ok[it][e]) pairs_local += so[it][e].n;
         }
     uint32_t pre = 0;
@@ -187,6 +216,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
           sb.spB[c] = make_float4(o.C, al[it], q2[it].y, q2[it].z);
           sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
           sb.count[c] = o.n;
+          sb.list_off[c] = loff[it][e];
           const uint32_t dk = __float_as_uint(o.depth);
           sb.spC[c] = make_float4(q2[it].w, o.thr, __uint_as_float(dk), 0.0f);
           sb.depth[c] = dk;

@@ -164,119 +164,8 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
   }
 }
 
-// ------------------------------------------------------------------ emit (a5)
-// Pairs (tile, splat) in depth order: sorted position p -> splat c; exclusive
-// scan of the kept-tile counts (decoupled look-back); the exact tile test of
-// project is re-evaluated to enumerate the kept tiles (identical arithmetic).
-constexpr int kEThreads = 256;
-constexpr int kEItems = 4;
-constexpr int kETile = 32 * kEItems;   // sorted positions per warp tile
-
-// Warp-centric and barrier-free: a warp acquires a tile of 128 sorted
-// positions, publishes its pair count, looks back, then walks its rounds.
-__global__ void __launch_bounds__(kEThreads)
-emit_kernel(EmitIn in, int width, int height, int TW, int Te, uint32_t cap, uint32_t *__restrict__ keys_out,
-            uint32_t *__restrict__ vals_out, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_hist[2][256];
-  __shared__ WarpTiles s_wt[kEThreads / 32];
-  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id(), lt = lanemask_lt();
-  for (int k = t; k < 512; k += kEThreads) (&s_hist[0][0])[k] = 0;
-  __syncthreads();
-  const uint32_t C = ctr->n_splat;
-  const uint32_t ntiles = (C + kETile - 1) / kETile;
-  WarpTiles &ws = s_wt[warp];
-  for (;;) {
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&ctr->tile_emit, 1u);
-    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
-    if (tile >= ntiles) break;
-    // round i, lane l -> sorted position tile*128 + i*32 + l
-    const uint32_t p0 = tile * kETile + lane;
-    uint32_t c[kEItems], cnt[kEItems], sum = 0;
-#pragma unroll
-    for (int i = 0; i < kEItems; ++i) {
-      uint32_t p = p0 + 32 * i;
-      c[i] = p < C ? in.sorted[p] : 0u;
-      cnt[i] = p < C ? in.count[c[i]] : 0u;
-      sum += cnt[i];
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xFFFFFFFFu, sum, o);
-    const uint32_t agg = sum;
-    uint32_t pre = 0;
-    if (tile == 0) {
-      if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
-    } else {
-      if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
-      pre = lookback_u32(status, tile);
-      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-    }
-    if (lane == 0 && tile == ntiles - 1) {
-      const uint32_t tot = pre + agg;
-      ctr->n_pairs = tot < cap ? tot : cap;
-      ctr->overflow = tot > cap;
-    }
-    uint32_t run = pre;
-#pragma unroll
-    for (int i = 0; i < kEItems; ++i) {
-      const bool has = cnt[i] > 0;
-      if (!__any_sync(0xFFFFFFFFu, has)) continue;
-      TileJob j{};
-      uint32_t kb = 0;
-      if (has) {
-        const uint32_t ci = c[i];
-        const float4 a = in.spA[ci];
-        const uint2 bx = in.box[ci];
-        j.u = a.x; j.v = a.y; j.A = a.z; j.B = a.w; j.C = in.spB[ci].x; j.thr = in.spC[ci].y;
-        j.tx0 = (int)(bx.x & 0xFFFFu); j.ty0 = (int)(bx.y & 0xFFFFu);
-        j.bw = (int)(bx.x >> 16) - j.tx0 + 1; j.bh = (int)((bx.y >> 16) & 0x7FFFu) - j.ty0 + 1;
-        kb = (bx.y >> 31) ? (uint32_t)Te : 0u;
-      }
-      ws.id[lane] = c[i];
-      ws.kb[lane] = kb;
-      const uint32_t total = warp_tiles_stage(ws, has, j, cnt[i]);
-      for (uint32_t w0 = 0; w0 < total; w0 += 32) {
-        const uint32_t w = w0 + lane;
-        int owner = 0, tx = 0, ty = 0;
-        const bool kept = w < total && warp_tiles_item(ws, w, width, height, owner, tx, ty);
-        const uint32_t mask = __ballot_sync(0xFFFFFFFFu, kept);
-        const uint32_t pos = run + __popc(mask & lt);
-        const uint32_t key = kept ? ws.kb[owner] + (uint32_t)(ty * TW + tx) : 0xFFFFFFFFu;
-        const bool wr = kept && pos < cap;
-        if (wr) {
-          keys_out[pos] = key;
-          vals_out[pos] = ws.id[owner];
-          atomicAdd(&s_hist[0][key & 0xFFu], 1u);
-        }
-        // high digit: mostly shared inside a warp step -> aggregate with match_any
-        const uint32_t hi = wr ? (key >> 8) & 0xFFu : 0x100u;
-        const uint32_t peers = __match_any_sync(0xFFFFFFFFu, hi);
-        if (wr && lane == (uint32_t)(__ffs(peers) - 1)) atomicAdd(&s_hist[1][hi], (uint32_t)__popc(peers));
-        run += __popc(mask);
-      }
-      __syncwarp();
-    }
-  }
-  __syncthreads();
-  for (int k = t; k < 512; k += kEThreads) {
-    uint32_t v = (&s_hist[0][0])[k];
-    if (v) atomicAdd(&ctr->hist_tile[0][0] + k, v);
-  }
-}
-
-// ------------------------------------------------------------------ ranges (a7)
-__global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *__restrict__ ctr,
-                              uint2 *__restrict__ ranges) {
-  const uint32_t P = ctr->n_pairs;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
-    uint32_t k = keys[p];
-    if (p == 0 || keys[p - 1] != k) ranges[k].x = p;
-    if (p == P - 1 || keys[p + 1] != k) ranges[k].y = p + 1;
-  }
-}
-
 // ------------------------------------------------------------------ launchers
-static int g_sort_grid = 0, g_emit_grid = 0;
+static int g_sort_grid = 0;
 
 static void sort_setup(int num_sms) {
   if (g_sort_grid) return;
@@ -310,21 +199,6 @@ void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint3
   }
 }
 
-void launch_emit(const EmitIn &in, int width, int height, int TW, int Te, uint32_t cap, uint32_t *keys_out,
-                 uint32_t *vals_out, uint32_t *status, FrameCounters *ctr, int num_sms, cudaStream_t st) {
-  if (!g_emit_grid) {
-    int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, emit_kernel, kEThreads, 0);
-    g_emit_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  emit_kernel<<<g_emit_grid, kEThreads, 0, st>>>(in, width, height, TW, Te, cap, keys_out, vals_out, status, ctr);
-}
-
-void launch_ranges(const uint32_t *keys, const FrameCounters *ctr, uint2 *ranges, int num_sms, cudaStream_t st) {
-  ranges_kernel<<<num_sms * 4, 256, 0, st>>>(keys, ctr, ranges);
-}
-
 int sort_tile_size() { return kSTile; }
-int emit_tile_size() { return kETile; }
 
 }  // namespace gsc
