@@ -434,6 +434,10 @@ int orc_tile_kept(const orc_config *cfg, const orc_splat *s, int tx, int ty) {
  * ====================================================================== */
 #define ORC_ALPHA_MIN 0.0039215688593685626983642578125f  /* fp32(1/255) = 0x3B808081 */
 
+/* N6: power = -1/2 (A dx^2 + 2 B dx dy + C dy^2) evaluated as
+ *   dx (a' dx + b' dy) + c' dy^2 with a' = -A/2, b' = -B, c' = -C/2, i.e.
+ *   q = fma(a', dx, b' dy); power = fma(dx, q, (c' dy) dy);
+ * T' = fma(-alpha', T, T) = T (1 - alpha'); C += c (alpha' T) by fma. */
 void orc_blend_pixel(const orc_splat *const *list, int n, float pxc, float pyc, const float bg[3],
                      float out[3], float *T_out, int *n_eval) {
   float T = 1.0f, C[3] = {0.0f, 0.0f, 0.0f};
@@ -442,17 +446,19 @@ void orc_blend_pixel(const orc_splat *const *list, int n, float pxc, float pyc, 
     const orc_splat *s = list[i];
     ++ev;
     float dx = s->u - pxc, dy = s->v - pyc;
-    float power = (-0.5f * ((s->A * (dx * dx)) + (s->C * (dy * dy)))) - (s->B * (dx * dy));
+    float a2 = -0.5f * s->A, b2 = -s->B, c2 = -0.5f * s->C;
+    float q = fmaf(a2, dx, b2 * dy);
+    float power = fmaf(dx, q, (c2 * dy) * dy);
     if (power > 0.0f) continue;
     float al = fminf(0.99f, s->alpha * orc_exp_s(power));
     if (al < ORC_ALPHA_MIN) continue;
-    float Tn = T * (1.0f - al);
+    float Tn = fmaf(-al, T, T);
     if (Tn < 0.0001f) break;
     float w = al * T;
-    for (int k = 0; k < 3; ++k) C[k] = C[k] + (s->rgb[k] * w);
+    for (int k = 0; k < 3; ++k) C[k] = fmaf(s->rgb[k], w, C[k]);
     T = Tn;
   }
-  for (int k = 0; k < 3; ++k) out[k] = C[k] + (T * bg[k]);
+  for (int k = 0; k < 3; ++k) out[k] = fmaf(T, bg[k], C[k]);
   if (T_out) *T_out = T;
   if (n_eval) *n_eval = ev;
 }

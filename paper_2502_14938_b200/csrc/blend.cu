@@ -24,7 +24,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
   __shared__ float4 sA[kBThreads];
   __shared__ float4 sB[kBThreads];
-  __shared__ float sb[kBThreads];
+  __shared__ float2 sC[kBThreads];
   const int t = threadIdx.x;
   const int tile = blockIdx.x;
   const int e = tile >= fc.Te;
@@ -44,30 +44,32 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
       uint32_t c = pair_vals[idx];
       sA[t] = spA[c];
       sB[t] = spB[c];
-      sb[t] = spC[c].x;
+      const float4 cc = spC[c];
+      sC[t] = make_float2(cc.x, cc.y);
     }
     __syncthreads();
     const int cnt = min((uint32_t)kBThreads, rg.y - b);
     if (!done) {
-      for (int k = 0; k < cnt; ++k) {
-        ++nev;
-        const float4 a = sA[k];
+      int k = 0;
+      for (; k < cnt; ++k) {
+        const float4 a = sA[k];     // (u, v, a' = -A/2, b' = -B)
+        const float4 q = sB[k];     // (c' = -C/2, skip bound, alpha, r)
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
-        const float4 q = sB[k];
-        const float power = __fsub_rn(
-            __fmul_rn(-0.5f, __fadd_rn(__fmul_rn(a.z, __fmul_rn(dx, dx)), __fmul_rn(q.x, __fmul_rn(dy, dy)))),
-            __fmul_rn(a.w, __fmul_rn(dx, dy)));
-        if (power > 0.0f || power < -5.55f) continue;
-        const float al = fminf(0.99f, __fmul_rn(q.y, exp_s(power)));
+        const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
+        const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
+        if (power < q.y || power > 0.0f) continue;
+        const float al = fminf(0.99f, __fmul_rn(q.z, exp_s(power)));
         if (al < kAlphaMin) continue;
-        const float Tn = __fmul_rn(T, __fsub_rn(1.0f, al));
+        const float Tn = __fmaf_rn(-al, T, T);
         if (Tn < 0.0001f) { done = 1; break; }
         const float w = __fmul_rn(al, T);
-        C0 = __fadd_rn(C0, __fmul_rn(q.z, w));
-        C1 = __fadd_rn(C1, __fmul_rn(q.w, w));
-        C2 = __fadd_rn(C2, __fmul_rn(sb[k], w));
+        const float2 gb = sC[k];
+        C0 = __fmaf_rn(q.w, w, C0);
+        C1 = __fmaf_rn(gb.x, w, C1);
+        C2 = __fmaf_rn(gb.y, w, C2);
         T = Tn;
       }
+      nev += (uint32_t)min(k + 1, cnt);
     }
     if (__syncthreads_count(done) == kBThreads) break;
   }
@@ -75,9 +77,9 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
   if ((t & 31) == 0 && nev) atomicAdd(&ctr->n_evals, (unsigned long long)nev);
   if (!inside) return;
-  const float o0 = __fadd_rn(C0, __fmul_rn(T, fc.bg[0]));
-  const float o1 = __fadd_rn(C1, __fmul_rn(T, fc.bg[1]));
-  const float o2 = __fadd_rn(C2, __fmul_rn(T, fc.bg[2]));
+  const float o0 = __fmaf_rn(T, fc.bg[0], C0);
+  const float o1 = __fmaf_rn(T, fc.bg[1], C1);
+  const float o2 = __fmaf_rn(T, fc.bg[2], C2);
   void *out = e ? out_r : out_l;
   const size_t HW = (size_t)fc.width * fc.height, pix = (size_t)py * fc.width + px;
   if (fmt == 0) {

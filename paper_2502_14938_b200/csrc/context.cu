@@ -631,7 +631,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       std::vector<uint64_t> out(np);
       for (size_t k = 0; k < np; ++k) {
         uint32_t db;
-        std::memcpy(&db, &C[pv[k]].z, 4);
+        std::memcpy(&db, &C[pv[k]].w, 4);
         out[k] = ((uint64_t)pk[k] << 32) | db;
       }
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
@@ -667,8 +667,9 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       CU(cudaMemcpy(cn.data(), ctx->count.p, ns * 4, cudaMemcpyDeviceToHost));
       std::vector<float> out(ns * 13);
       for (size_t k = 0; k < ns; ++k) {
-        float r[13] = {A[k].x, A[k].y, A[k].z, A[k].w, B[k].x, B[k].y, B[k].z, B[k].w, Cc[k].x, Cc[k].z, Cc[k].y,
-                       (float)(bx[k].y >> 31), (float)cn[k]};
+        // records hold (u, v, -A/2, -B), (-C/2, bound, alpha, r), (g, b, thr, depth); -2 x (-A/2) is exact
+        float r[13] = {A[k].x, A[k].y, -2.0f * A[k].z, -A[k].w, -2.0f * B[k].x, B[k].z, B[k].w, Cc[k].x, Cc[k].y,
+                       Cc[k].w, Cc[k].z, (float)(bx[k].y >> 31), (float)cn[k]};
         std::memcpy(&out[13 * k], r, sizeof(r));
       }
       std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));

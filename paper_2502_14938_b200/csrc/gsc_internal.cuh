@@ -60,9 +60,9 @@ struct PolicyState {
 
 // compacted splat records (index c), written by project, read by emit/blend
 struct SplatBufs {
-  float4 *spA;       // (u, v, A, B)       A,B,C = conic (A dx^2 + 2B dx dy + C dy^2)
-  float4 *spB;       // (C, alpha, r, g)
-  float4 *spC;       // (b, thr, depth, 0)
+  float4 *spA;       // (u, v, -A/2, -B)     A,B,C = conic (A dx^2 + 2B dx dy + C dy^2)
+  float4 *spB;       // (-C/2, skip bound, alpha, r)
+  float4 *spC;       // (g, b, thr, depth)
   uint2 *box;        // candidate tile box: tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
   uint32_t *count;   // kept tiles
   uint32_t *depth;   // depth key = bits(z) (depth-sort input)

@@ -212,13 +212,16 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
         if (ok[it][e]) {
           const SplatOut &o = so[it][e];
           const uint32_t c = base + __popc(m[e][it] & lt);
-          sb.spA[c] = make_float4(o.u, o.v, o.A, o.B);
-          sb.spB[c] = make_float4(o.C, al[it], q2[it].y, q2[it].z);
+          // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, thr, depth)
+          // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
+          const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+          sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
+          sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al[it], q2[it].y);
           sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
           sb.count[c] = o.n;
           sb.list_off[c] = loff[it][e];
           const uint32_t dk = __float_as_uint(o.depth);
-          sb.spC[c] = make_float4(q2[it].w, o.thr, __uint_as_float(dk), 0.0f);
+          sb.spC[c] = make_float4(q2[it].z, q2[it].w, o.thr, __uint_as_float(dk));
           sb.depth[c] = dk;
           sb.gslot[c] = gs[it];
 #pragma unroll
