@@ -401,8 +401,9 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
 }
 
 /* min over t in [lo,hi] of P d^2 + 2 Q d t + R t^2, clamped minimiser t* = -Q d / R */
+/* R14: the clamped minimiser uses the reciprocal of R rounded once: t* = -(Q d) * fl(1/R) */
 static inline float edge_q(float d, float lo, float hi, float P, float Q, float R) {
-  float t = -(Q * d) / R;
+  float t = -(Q * d) * (1.0f / R);
   t = fminf(fmaxf(t, lo), hi);
   return ((P * (d * d)) + (2.0f * (Q * (d * t)))) + (R * (t * t));
 }

@@ -131,13 +131,39 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   }
 }
 
+// 4 keys per thread (one 16-byte load); neighbours across the vector boundary
+// come from the adjacent lane or, at warp edges, one extra cached load.
 __global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *__restrict__ ctr,
                               uint2 *__restrict__ ranges) {
   const uint32_t P = ctr->n_pairs;
-  for (uint32_t p = blockIdx.x * blockDim.x + threadIdx.x; p < P; p += gridDim.x * blockDim.x) {
-    const uint32_t k = keys[p];
-    if (p == 0 || keys[p - 1] != k) ranges[k].x = p;
-    if (p == P - 1 || keys[p + 1] != k) ranges[k].y = p + 1;
+  const uint32_t nvec = (P + 3) / 4;
+  const uint32_t lane = lane_id();
+  const uint32_t stride = gridDim.x * blockDim.x;
+  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < nvec; v0 += stride) {
+    const uint32_t v = v0 + threadIdx.x;
+    const uint32_t p = 4 * v;
+    uint32_t k[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
+    if (p + 3 < P) {
+      const uint4 q = reinterpret_cast<const uint4 *>(keys)[v];
+      k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
+    } else {
+      for (int i = 0; i < 4; ++i)
+        if (p + i < P) k[i] = keys[p + i];
+    }
+    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, k[3], 1);
+    uint32_t next = __shfl_down_sync(0xFFFFFFFFu, k[0], 1);
+    if (lane == 0) prev = p > 0 && p - 1 < P ? keys[p - 1] : 0xFFFFFFFEu;
+    if (lane == 31) next = p + 4 < P ? keys[p + 4] : 0xFFFFFFFEu;
+    if (p >= P) continue;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const uint32_t q = p + i;
+      if (q >= P) break;
+      const uint32_t before = i == 0 ? prev : k[i - 1];
+      const uint32_t after = (i == 3 || q + 1 >= P) ? (q + 1 >= P ? 0xFFFFFFFEu : next) : k[i + 1];
+      if (q == 0 || before != k[i]) ranges[k[i]].x = q;
+      if (after != k[i]) ranges[k[i]].y = q + 1;
+    }
   }
 }
 

@@ -98,6 +98,7 @@ __device__ __forceinline__ uint32_t warp_count_list(WarpTiles &ws, bool has, con
   j.tx0 = (int)(o.box_x & 0xFFFFu); j.ty0 = (int)(o.box_y & 0xFFFFu);
   j.bw = (int)(o.box_x >> 16) - j.tx0 + 1; j.bh = (int)((o.box_y >> 16) & 0x7FFFu) - j.ty0 + 1;
   const uint32_t lane = lane_id(), lt = lanemask_lt();
+  ws.kb[lane] = kb;   // key base of the lane's eye; items are keyed with their OWNER's base
   const uint32_t total = warp_tiles_stage(ws, has, j, 0xFFFFFFFFu);
   uint32_t base = 0;
   if (lane == 0) {
@@ -114,7 +115,7 @@ __device__ __forceinline__ uint32_t warp_count_list(WarpTiles &ws, bool has, con
     if (kept) {
       atomicAdd(&ws.cnt[owner], 1u);
       const uint32_t pos = run + __popc(mask & lt);
-      if (pos < list_cap) list[pos] = kb + (uint32_t)(ty * TW + tx);
+      if (pos < list_cap) list[pos] = ws.kb[owner] + (uint32_t)(ty * TW + tx);
     }
     run += __popc(mask);
   }
@@ -136,14 +137,11 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
                const float4 *__restrict__ pool, SplatBufs sb, uint32_t *__restrict__ status,
                FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_hist[4][256];
-  __shared__ WarpTiles s_wt[kPThreads / 32];
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
   __syncthreads();
   const uint32_t S = ctr->n_visible * (uint32_t)kK;
   const uint32_t ntiles = (S + kPTile - 1) / kPTile;
-  WarpTiles &ws = s_wt[warp];
-  uint32_t pairs_local = 0;
 
   for (;;) {
     uint32_t tile = 0;
@@ -152,14 +150,18 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
     if (tile >= ntiles) break;
 
     SplatOut so[kPItems][2];
-    bool ok[kPItems][2];
+    bool ok[kPItems][2], live[kPItems];
     uint32_t gs[kPItems];
     float4 q2[kPItems];
     float al[kPItems];
+    // compaction is over LIVE slots (255 alpha > 1), both eyes: the tile's
+    // aggregate is known after the 4-byte alpha reads and is published before
+    // the projection math, so the look-back never waits on a predecessor's
+    // arithmetic.  Live splats that project nowhere keep an entry with 0 tiles.
+    uint32_t m[kPItems], agg = 0;
 #pragma unroll
     for (int it = 0; it < kPItems; ++it) {
       const uint32_t s = tile * kPTile + it * 32 + lane;
-      ok[it][0] = ok[it][1] = false;
       al[it] = 0.0f;
       gs[it] = 0;
       if (s < S) {
@@ -167,37 +169,25 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
         uint32_t g = visible[v] * kK + j;
         gs[it] = g;
         al[it] = alpha[g];
-        if (__fmul_rn(255.0f, al[it]) > 1.0f) {
-          const float4 q0 = pool[3 * (size_t)g];
-          const float4 q1 = pool[3 * (size_t)g + 1];
-          q2[it] = pool[3 * (size_t)g + 2];
+      }
+      live[it] = __fmul_rn(255.0f, al[it]) > 1.0f;
+      m[it] = __ballot_sync(0xFFFFFFFFu, live[it]);
+      agg += 2 * __popc(m[it]);
+    }
+    if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
 #pragma unroll
-          for (int e = 0; e < 2; ++e)
-            ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0, q1, q2[it], so[it][e]);
-        }
+    for (int it = 0; it < kPItems; ++it) {
+      ok[it][0] = ok[it][1] = false;
+      if (live[it]) {
+        const size_t g = gs[it];
+        const float4 q0 = pool[3 * g];
+        const float4 q1 = pool[3 * g + 1];
+        q2[it] = pool[3 * g + 2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+          ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0, q1, q2[it], so[it][e]);
       }
     }
-    // compaction masks in (eye, item, lane) order; publish the aggregate early
-    uint32_t m[2][kPItems], agg = 0;
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int it = 0; it < kPItems; ++it) {
-        m[e][it] = __ballot_sync(0xFFFFFFFFu, ok[it][e]);
-        agg += __popc(m[e][it]);
-      }
-    if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-    // kept-tile counts and lists (the expensive part) while predecessors publish
-    uint32_t loff[kPItems][2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int it = 0; it < kPItems; ++it)
-        if (m[e][it]) {
-          so[it][e].n = warp_count_list(ws, ok[it][e], so[it][e], e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
-                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff[it][e]);
-          if (ok[it][e]) pairs_local += so[it][e].n;
-        }
     uint32_t pre = 0;
     if (tile > 0) {
       pre = lookback_u32(status, tile);
@@ -209,30 +199,31 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
     for (int e = 0; e < 2; ++e)
 #pragma unroll
       for (int it = 0; it < kPItems; ++it) {
-        if (ok[it][e]) {
+        if (live[it]) {
           const SplatOut &o = so[it][e];
-          const uint32_t c = base + __popc(m[e][it] & lt);
-          // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, thr, depth)
-          // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
-          const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
-          sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
-          sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al[it], q2[it].y);
-          sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-          sb.count[c] = o.n;
-          sb.list_off[c] = loff[it][e];
-          const uint32_t dk = __float_as_uint(o.depth);
-          sb.spC[c] = make_float4(q2[it].z, q2[it].w, o.thr, __uint_as_float(dk));
+          const uint32_t c = base + __popc(m[it] & lt);
+          uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
+          if (ok[it][e]) {
+            // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, thr, depth)
+            // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
+            const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+            dk = __float_as_uint(o.depth);
+            sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
+            sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al[it], q2[it].y);
+            sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
+            sb.spC[c] = make_float4(q2[it].z, q2[it].w, o.thr, __uint_as_float(dk));
+          } else {
+            sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
+          }
           sb.depth[c] = dk;
           sb.gslot[c] = gs[it];
 #pragma unroll
           for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
         }
-        base += __popc(m[e][it]);
+        base += __popc(m[it]);
       }
   }
-  // flush the fused histogram and the pair count
-  for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
-  if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
+  // flush the fused histogram
   __syncthreads();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) {
     uint32_t v = (&s_hist[0][0])[k];
@@ -240,7 +231,46 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
   }
 }
 
-static int g_project_grid = 0;
+// Exact tile test of every candidate tile of every compacted splat
+// (warp-flattened over 32 splats at a time) -> kept count and the kept-tile
+// list (row-major keys eye*T_e + ty*TW + tx).  No ordering constraint: each
+// warp bump-allocates its list space.
+__global__ void __launch_bounds__(kPThreads)
+tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
+  __shared__ WarpTiles s_wt[kPThreads / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  WarpTiles &ws = s_wt[warp];
+  const uint32_t C = ctr->n_splat;
+  const uint32_t nw = (gridDim.x * kPThreads) >> 5;
+  uint32_t pairs_local = 0;
+  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 32 + warp * 32; base < C; base += nw * 32) {
+    const uint32_t c = base + lane;
+    const bool in = c < C;
+    const uint2 bx = in ? sb.box[c] : make_uint2(0x0000FFFFu, 0u);
+    const bool has = (bx.x >> 16) >= (bx.x & 0xFFFFu);     // dead entries carry an empty box
+    SplatOut o{};
+    uint32_t kb = 0;
+    if (has) {
+      const float4 a = sb.spA[c];
+      o.u = a.x; o.v = a.y; o.A = __fmul_rn(-2.0f, a.z); o.B = -a.w;
+      o.C = __fmul_rn(-2.0f, sb.spB[c].x); o.thr = sb.spC[c].z;
+      o.box_x = bx.x; o.box_y = bx.y & 0x7FFFFFFFu;
+      kb = (bx.y >> 31) ? (uint32_t)fc.Te : 0u;
+    }
+    uint32_t loff = 0;
+    const uint32_t n = warp_count_list(ws, has, o, kb, fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
+                                       &ctr->list_top, &ctr->overflow, loff);
+    if (in) {
+      sb.count[c] = n;
+      sb.list_off[c] = loff;
+      pairs_local += n;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
+  if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
+}
+
+static int g_project_grid = 0, g_tiles_grid = 0;
 
 void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
                     const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms, cudaStream_t st) {
@@ -248,8 +278,11 @@ void launch_project(const FrameC &fc, const uint32_t *visible, const float *alph
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel, kPThreads, 0);
     g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_kernel, kPThreads, 0);
+    g_tiles_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
   project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, visible, alpha, pool, sb, status, ctr);
+  tiles_kernel<<<g_tiles_grid, kPThreads, 0, st>>>(fc, sb, ctr);
 }
 int project_tile_size() { return kPTile; }
 
