@@ -176,17 +176,19 @@ def run_gsc(args):
         for s in stages:
             algo[s] += b[s]
     evals = sum(h["n_evals"] for h in hist)
+    nexp = sum(h["n_exp"] for h in hist)
     peaks = _peaks()
     dom = max(stages, key=lambda s: ms[s])
     if dom == "blend":
-        # ALU bound: FP32 instructions of the per-(pixel, splat) evaluation
-        ops = evals * BLEND_OPS_PER_EVAL
+        # ALU bound: fp32-pipe instructions of the evaluations actually executed
+        ops = evals * BLEND_OPS_PER_EVAL + nexp * BLEND_OPS_PER_EXP
         peak = 148 * 128 * peaks["sm_max_mhz"] * 1e6 / 1e12
         achieved = ops / (ms[dom] / 1000.0) / 1e12
         roof = {"kernel": "blend", "bound": "alu", "achieved": round(achieved, 3), "peak": round(peak, 2),
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": None,
-                "note": f"{BLEND_OPS_PER_EVAL} fp32 ops per evaluation x {evals / nf:.3g} evaluations/frame; "
-                        "peak = 148 SMs x 128 fp32 lanes x max SM clock"}
+                "note": f"fp32-pipe instructions: {BLEND_OPS_PER_EVAL}/evaluation x {evals / nf:.3g} evaluations/frame "
+                        f"+ {BLEND_OPS_PER_EXP}/exp-path x {nexp / nf:.3g}; peak = 148 SMs x 128 fp32 lanes x "
+                        "max SM clock (1 instruction/lane/clock)"}
     else:
         achieved = algo[dom] / (ms[dom] / 1000.0) / 1e9
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
@@ -218,7 +220,7 @@ def run_gsc(args):
                              "misses": round(sum(h["n_misses"] for h in hist) / nf),
                              "splats": round(sum(h["n_splats"] for h in hist) / nf),
                              "pairs": round(sum(h["n_pairs"] for h in hist) / nf),
-                             "evals": round(evals / nf), "overflow": overflow},
+                             "evals": round(evals / nf), "exp_evals": round(nexp / nf), "overflow": overflow},
             "roofline": roof,
             "e2e": {"value": round(total_frames / e2e_max, 3) if e2e_max > 0 else None, "unit": UNIT,
                     "h2d_bytes_per_step": 120, "d2h_bytes_per_step": 2 * cfg.width * cfg.height * 4},
@@ -230,7 +232,8 @@ def run_gsc(args):
         print(json.dumps(line), flush=True)
 
 
-BLEND_OPS_PER_EVAL = 11   # dx, dy, dx^2, dy^2, dx*dy, A*, C*, B*, +, *(-1/2), -  (minimum per evaluation)
+BLEND_OPS_PER_EVAL = 7    # dx, dy, b'dy, fma(a',dx,.), c'dy, (.)dy, fma(dx,q,.)  (N6 power)
+BLEND_OPS_PER_EXP = 24    # exp_core (15) + alpha', clamp, tests, T', w, 3 colour fma (9)
 
 
 def cpu_baseline(cfg, sc, traj, frames):

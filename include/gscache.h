@@ -104,7 +104,8 @@ typedef struct {
   float update_rate, novelty_rate;               /* misses/|X_f|, new/|X_f| */
   /* stage times in ms (GSC_F_STAGE_TIMING; else 0): */
   float ms_cull, ms_derive, ms_project, ms_depth_sort, ms_emit, ms_tile_sort, ms_ranges, ms_blend, ms_total;
-  uint64_t n_evals;                              /* blend: per-pixel splat evaluations */
+  uint64_t n_evals;                              /* blend: (pixel, splat) evaluations executed */
+  uint64_t n_exp;                                /* blend: evaluations inside the skip bound (exp evaluated) */
 } gsc_frame_stats;
 
 /* out formats */

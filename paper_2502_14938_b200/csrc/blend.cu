@@ -1,17 +1,20 @@
 // blend.cu -- SURVEY §8(a) row a8: per-tile front-to-back alpha compositing
 // for both eyes (Eq. 1; Alg. 1; reading R17).
 //
-// One 256-thread CTA per (eye, 16x16 tile), one pixel per thread; the tile's
-// depth-sorted splats are staged through shared memory in batches of 256
-// (36 bytes each: float4 (u,v,A,B), float4 (C,alpha,r,g), float b); the CTA
-// leaves as soon as every pixel of the tile has terminated
-// (__syncthreads_count).  Per (pixel, splat), in the exact op order of
-// DESIGN.md Numerics N6:
-//   power = -0.5 (A dx^2 + C dy^2) - B dx dy      (skip if > 0)
-//   alpha' = min(0.99, alpha exp_s(power))        (skip if < 1/255)
-//   T' = T (1 - alpha'); stop before T' < 1e-4; C += c (alpha' T); T = T'
-// power < -5.55 is skipped without evaluating exp_s: exp_s(-5.55) < 1/255
-// and alpha <= 1, so the skip decision is identical (N5).
+// One 256-thread CTA per (eye, 16x16 tile), one pixel per thread; warp w owns
+// the 16x2 pixel strip of rows 2w, 2w+1.  The tile's depth-sorted splats are
+// staged through shared memory in batches of 256 (40 bytes each); while
+// staging, each thread also computes an 8-bit strip mask: bit w is set unless
+// the padded bounding box of {power >= skip bound} misses strip w.  A warp
+// then walks only the batch entries of its strip (ballot + ffs), stops as
+// soon as all its 32 pixels have terminated, and the CTA leaves when all 256
+// have (__syncthreads_count).  Skipping a (pixel, splat) this way never
+// changes a decision: outside that box power < -ln(255 alpha) - 2^-7, so
+// alpha' < 1/255 (N5).  Per evaluated (pixel, splat), the exact op
+// order of DESIGN.md N6 (identical in the oracle):
+//   power  = fma(dx, fma(a', dx, b' dy), (c' dy) dy)      (skip if > 0)
+//   alpha' = min(0.99, alpha exp_s(power))                (skip if < 1/255)
+//   T' = fma(-alpha', T, T); stop before T' < 1e-4; C = fma(c, alpha' T, C)
 #include "gsc_internal.cuh"
 
 namespace gsc {
@@ -25,7 +28,9 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   __shared__ float4 sA[kBThreads];
   __shared__ float4 sB[kBThreads];
   __shared__ float2 sC[kBThreads];
+  __shared__ uint32_t sM[kBThreads];
   const int t = threadIdx.x;
+  const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
   const int e = tile >= fc.Te;
   const int tl = tile - e * fc.Te;
@@ -33,35 +38,54 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const int px = tx * kTile + (t & 15), py = ty * kTile + (t >> 4);
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
+  const float X0 = __fadd_rn((float)(tx * kTile), 0.5f), X1 = __fadd_rn(X0, 15.0f);
+  const float Yb = __fadd_rn((float)(ty * kTile), 0.5f);
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int done = !inside;
-  uint32_t nev = 0;
+  uint32_t nev = 0, nexp = 0;
   for (uint32_t b = rg.x; b < rg.y; b += kBThreads) {
     __syncthreads();
-    uint32_t idx = b + t;
+    const uint32_t idx = b + t;
     if (idx < rg.y) {
-      uint32_t c = pair_vals[idx];
-      sA[t] = spA[c];
-      sB[t] = spB[c];
+      const uint32_t c = pair_vals[idx];
+      const float4 a = spA[c];
       const float4 cc = spC[c];
+      sA[t] = a;
+      sB[t] = spB[c];
       sC[t] = make_float2(cc.x, cc.y);
+      uint32_t mask = 0;
+      if (__fadd_rn(a.x, cc.z) >= X0 && __fsub_rn(a.x, cc.z) <= X1) {
+        const float lo = __fsub_rn(a.y, cc.w), hi = __fadd_rn(a.y, cc.w);
+#pragma unroll
+        for (int w = 0; w < 8; ++w) {
+          const float y0 = __fadd_rn(Yb, (float)(2 * w));
+          if (hi >= y0 && lo <= __fadd_rn(y0, 1.0f)) mask |= 1u << w;
+        }
+      }
+      sM[t] = mask;
     }
     __syncthreads();
     const int cnt = min((uint32_t)kBThreads, rg.y - b);
-    if (!done) {
-      int k = 0;
-      for (; k < cnt; ++k) {
+    for (int c0 = 0; c0 < cnt; c0 += 32) {
+      if (__all_sync(0xFFFFFFFFu, done)) break;
+      uint32_t bits = __ballot_sync(0xFFFFFFFFu, c0 + (int)lane < cnt && ((sM[c0 + lane] >> warp) & 1u));
+      while (bits) {
+        const int k = c0 + __ffs(bits) - 1;
+        bits &= bits - 1;
+        if (done) continue;
+        ++nev;
         const float4 a = sA[k];     // (u, v, a' = -A/2, b' = -B)
         const float4 q = sB[k];     // (c' = -C/2, skip bound, alpha, r)
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
         const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
         if (power < q.y || power > 0.0f) continue;
-        const float al = fminf(0.99f, __fmul_rn(q.z, exp_s(power)));
+        ++nexp;
+        const float al = fminf(0.99f, __fmul_rn(q.z, exp_core(power)));   // power in [-5.6, 0]
         if (al < kAlphaMin) continue;
         const float Tn = __fmaf_rn(-al, T, T);
-        if (Tn < 0.0001f) { done = 1; break; }
+        if (Tn < 0.0001f) { done = 1; continue; }
         const float w = __fmul_rn(al, T);
         const float2 gb = sC[k];
         C0 = __fmaf_rn(q.w, w, C0);
@@ -69,13 +93,18 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
         C2 = __fmaf_rn(gb.y, w, C2);
         T = Tn;
       }
-      nev += (uint32_t)min(k + 1, cnt);
     }
     if (__syncthreads_count(done) == kBThreads) break;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
-  if ((t & 31) == 0 && nev) atomicAdd(&ctr->n_evals, (unsigned long long)nev);
+  for (int o = 16; o > 0; o >>= 1) {
+    nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
+    nexp += __shfl_xor_sync(0xFFFFFFFFu, nexp, o);
+  }
+  if (lane == 0 && nev) {
+    atomicAdd(&ctr->n_evals, (unsigned long long)nev);
+    atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
+  }
   if (!inside) return;
   const float o0 = __fmaf_rn(T, fc.bg[0], C0);
   const float o1 = __fmaf_rn(T, fc.bg[1], C1);

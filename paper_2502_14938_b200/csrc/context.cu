@@ -95,6 +95,7 @@ struct gsc_ctx {
   DevBuf<uint32_t> visible, misses;
   size_t cap_splat = 0, cap_pairs = 0;
   DevBuf<float4> spA, spB, spC;
+  DevBuf<float2> spD;
   DevBuf<uint2> box;
   DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list;
   DevBuf<uint32_t> pkey_a, pval_a, pkey_b, pval_b;
@@ -296,6 +297,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->spA.alloc(ctx->cap_splat));
   CU(ctx->spB.alloc(ctx->cap_splat));
   CU(ctx->spC.alloc(ctx->cap_splat));
+  CU(ctx->spD.alloc(ctx->cap_splat));
   CU(ctx->box.alloc(ctx->cap_splat));
   CU(ctx->count.alloc(ctx->cap_splat));
   CU(ctx->gslot.alloc(ctx->cap_splat));
@@ -421,7 +423,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
                 ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, st);
   mark();
   // a4
-  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
+  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
                ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
   launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, sb,
                  reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
@@ -469,6 +471,7 @@ static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
   s->n_pairs = r.n_pairs_raw;
   s->overflow = r.overflow;
   s->n_evals = r.n_evals;
+  s->n_exp = r.n_exp;
   s->depth_used = r.depth_used;
   s->depth_next = r.depth_next;
   s->update_rate = r.n_visible ? (float)r.n_miss / (float)r.n_visible : 0.0f;
@@ -624,14 +627,14 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       *len = np * 8;
       if (!host_dst || !cap) return GSC_OK;
       std::vector<uint32_t> pk(np), pv(np);
-      std::vector<float4> C(ns);
+      std::vector<float2> D(ns);
       CU(cudaMemcpy(pk.data(), ctx->pkey_a.p, np * 4, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(pv.data(), ctx->pval_a.p, np * 4, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(C.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
       std::vector<uint64_t> out(np);
       for (size_t k = 0; k < np; ++k) {
         uint32_t db;
-        std::memcpy(&db, &C[pv[k]].w, 4);
+        std::memcpy(&db, &D[pv[k]].y, 4);
         out[k] = ((uint64_t)pk[k] << 32) | db;
       }
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
@@ -658,18 +661,21 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       *len = ns * 13 * 4;
       if (!host_dst || !cap) return GSC_OK;
       std::vector<float4> A(ns), B(ns), Cc(ns);
+      std::vector<float2> D(ns);
       std::vector<uint2> bx(ns);
       std::vector<uint32_t> cn(ns);
       CU(cudaMemcpy(A.data(), ctx->spA.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(B.data(), ctx->spB.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(Cc.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(bx.data(), ctx->box.p, ns * 8, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(cn.data(), ctx->count.p, ns * 4, cudaMemcpyDeviceToHost));
       std::vector<float> out(ns * 13);
       for (size_t k = 0; k < ns; ++k) {
-        // records hold (u, v, -A/2, -B), (-C/2, bound, alpha, r), (g, b, thr, depth); -2 x (-A/2) is exact
+        // records hold (u, v, -A/2, -B), (-C/2, bound, alpha, r), (g, b, rx, ry), (thr, depth);
+        // -2 x (-A/2) is exact
         float r[13] = {A[k].x, A[k].y, -2.0f * A[k].z, -A[k].w, -2.0f * B[k].x, B[k].z, B[k].w, Cc[k].x, Cc[k].y,
-                       Cc[k].w, Cc[k].z, (float)(bx[k].y >> 31), (float)cn[k]};
+                       D[k].y, D[k].x, (float)(bx[k].y >> 31), (float)cn[k]};
         std::memcpy(&out[13 * k], r, sizeof(r));
       }
       std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));

@@ -163,6 +163,7 @@ __global__ void record_kernel(const FrameCounters *ctr, FrameRecordDev *rec) {
   rec->n_pairs_raw = ctr->n_pairs_raw;
   rec->overflow = ctr->overflow;
   rec->n_evals = ctr->n_evals;
+  rec->n_exp = ctr->n_exp;
 }
 
 // load-time: m_i = max_j |O_ij (.) s_i|_2 + 3.33 max_k s_ik  (R8), packed with pos

@@ -42,7 +42,8 @@ struct FrameCounters {
   uint32_t n_pairs;            // min(raw, capacity)
   uint32_t overflow;
   uint32_t list_top;           // project: bump allocator of the kept-tile list
-  unsigned long long n_evals;  // blend: per-pixel splat evaluations
+  unsigned long long n_evals;  // blend: (pixel, splat) evaluations executed
+  unsigned long long n_exp;    // blend: evaluations that reached exp_s
   uint32_t tile_pairoff, tile_expand, pad2[2];
   uint32_t hist_depth[4][256];
   uint32_t hist_tile[2][256];
@@ -62,7 +63,8 @@ struct PolicyState {
 struct SplatBufs {
   float4 *spA;       // (u, v, -A/2, -B)     A,B,C = conic (A dx^2 + 2B dx dy + C dy^2)
   float4 *spB;       // (-C/2, skip bound, alpha, r)
-  float4 *spC;       // (g, b, thr, depth)
+  float4 *spC;       // (g, b, rx, ry): colour and the half-extents of {power >= skip bound} (blend strip cull)
+  float2 *spD;       // (thr, depth)
   uint2 *box;        // candidate tile box: tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
   uint32_t *count;   // kept tiles
   uint32_t *depth;   // depth key = bits(z) (depth-sort input)
@@ -84,7 +86,7 @@ struct EmitIn {
 struct FrameRecordDev {
   int32_t frame, depth_used, depth_next, pad0;
   uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, pad1, pad2;
-  unsigned long long n_evals;
+  unsigned long long n_evals, n_exp;
 };
 
 // ---------------------------------------------------------------- helpers
@@ -167,6 +169,25 @@ __device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *s
 // ---------------------------------------------------------------- elementary functions
 // DESIGN.md Numerics N1-N4.  Independent implementation of the same op
 // sequence the oracle uses; __fmaf_rn only where the definition says fma.
+// exp_s without the special-value branches; identical to exp_s on [-87.33654, 88.0]
+__device__ __forceinline__ float exp_core(float x) {
+  const float log2e = 1.44269502162933349609375f;
+  const float ln2_hi = 0.693145751953125f;
+  const float ln2_lo = 1.428606765330187045037746429443359375e-06f;
+  float n = rintf(__fmul_rn(x, log2e));
+  float r = __fsub_rn(x, __fmul_rn(n, ln2_hi));
+  r = __fsub_rn(r, __fmul_rn(n, ln2_lo));
+  float p = 1.98412698e-04f;
+  p = __fmaf_rn(p, r, 1.38888889e-03f);
+  p = __fmaf_rn(p, r, 8.33333377e-03f);
+  p = __fmaf_rn(p, r, 4.16666679e-02f);
+  p = __fmaf_rn(p, r, 1.66666672e-01f);
+  p = __fmaf_rn(p, r, 0.5f);
+  p = __fmaf_rn(p, r, 1.0f);
+  p = __fmaf_rn(p, r, 1.0f);
+  return __fmul_rn(p, __uint_as_float((uint32_t)(__float2int_rz(n) + 127) << 23));
+}
+
 __device__ __forceinline__ float exp_s(float x) {
   if (x != x) return x;
   if (x > 88.72283935546875f) return __int_as_float(0x7F800000);

@@ -23,6 +23,7 @@ constexpr int kPTile = 32 * kPItems;   // slots per warp tile
 
 struct SplatOut {
   float u, v, A, B, C, thr;
+  float sxx, syy;          // 2D covariance diagonal (after the 0.3 floor)
   uint32_t box_x, box_y;   // tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
   uint32_t n;
   float depth;
@@ -63,6 +64,8 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   c = __fadd_rn(c, 0.3f);
   float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));
   if (!(det > 0.0f)) return false;
+  o.sxx = a;
+  o.syy = c;
   o.A = __fdiv_rn(c, det);
   o.B = __fdiv_rn(-b, det);
   o.C = __fdiv_rn(a, det);
@@ -211,7 +214,13 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
             sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
             sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al[it], q2[it].y);
             sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-            sb.spC[c] = make_float4(q2[it].z, q2[it].w, o.thr, __uint_as_float(dk));
+            // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
+            // outside them has power < pmin, so the blend may skip it without changing a decision
+            const float qmax = __fmul_rn(-2.0f, pmin);
+            const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
+            const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
+            sb.spC[c] = make_float4(q2[it].z, q2[it].w, rx, ry);
+            sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
           } else {
             sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
           }
@@ -253,7 +262,7 @@ tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
     if (has) {
       const float4 a = sb.spA[c];
       o.u = a.x; o.v = a.y; o.A = __fmul_rn(-2.0f, a.z); o.B = -a.w;
-      o.C = __fmul_rn(-2.0f, sb.spB[c].x); o.thr = sb.spC[c].z;
+      o.C = __fmul_rn(-2.0f, sb.spB[c].x); o.thr = sb.spD[c].x;
       o.box_x = bx.x; o.box_y = bx.y & 0x7FFFFFFFu;
       kb = (bx.y >> 31) ? (uint32_t)fc.Te : 0u;
     }
