@@ -21,6 +21,23 @@ namespace gsc {
 
 constexpr int kBThreads = 256;
 
+// explicit 32-bit shared-window loads (keeps the window base out of the hot loop)
+__device__ __forceinline__ float4 lds_f4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ float2 lds_f2(uint32_t a) {
+  float2 v;
+  asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
+  unsigned short v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+  return v;
+}
+
 __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
@@ -29,6 +46,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   __shared__ float4 sB[kBThreads];
   __shared__ float2 sC[kBThreads];
   __shared__ uint32_t sM[kBThreads];
+  __shared__ uint16_t sL[kBThreads / 32][kBThreads];
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
@@ -67,16 +85,28 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     }
     __syncthreads();
     const int cnt = min((uint32_t)kBThreads, rg.y - b);
-    for (int c0 = 0; c0 < cnt; c0 += 32) {
-      if (__all_sync(0xFFFFFFFFu, done)) break;
-      uint32_t bits = __ballot_sync(0xFFFFFFFFu, c0 + (int)lane < cnt && ((sM[c0 + lane] >> warp) & 1u));
-      while (bits) {
-        const int k = c0 + __ffs(bits) - 1;
-        bits &= bits - 1;
+    if (!__all_sync(0xFFFFFFFFu, done)) {
+      // this warp's strip list (batch indices in depth order)
+      int n = 0;
+      for (int c0 = 0; c0 < cnt; c0 += 32) {
+        const bool in = c0 + (int)lane < cnt && ((sM[c0 + lane] >> warp) & 1u);
+        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
+        if (in) sL[warp][n + __popc(bits & lanemask_lt())] = (uint16_t)(c0 + lane);
+        n += __popc(bits);
+      }
+      __syncwarp();
+      uint32_t aA = (uint32_t)__cvta_generic_to_shared(sA), aB = (uint32_t)__cvta_generic_to_shared(sB);
+      uint32_t aC = (uint32_t)__cvta_generic_to_shared(sC);
+      uint32_t aL = (uint32_t)__cvta_generic_to_shared(&sL[warp][0]);
+      // opaque to the compiler: keeps the addresses in registers instead of re-deriving the window base
+      asm volatile("" : "+r"(aA), "+r"(aB), "+r"(aC), "+r"(aL));
+      for (int i = 0; i < n; ++i) {
+        if ((i & 7) == 0 && __all_sync(0xFFFFFFFFu, done)) break;
         if (done) continue;
+        const uint32_t k = lds_u16(aL + 2 * i);
         ++nev;
-        const float4 a = sA[k];     // (u, v, a' = -A/2, b' = -B)
-        const float4 q = sB[k];     // (c' = -C/2, skip bound, alpha, r)
+        const float4 a = lds_f4(aA + 16 * k);     // (u, v, a' = -A/2, b' = -B)
+        const float4 q = lds_f4(aB + 16 * k);     // (c' = -C/2, skip bound, alpha, r)
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
         const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
@@ -87,7 +117,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
         const float Tn = __fmaf_rn(-al, T, T);
         if (Tn < 0.0001f) { done = 1; continue; }
         const float w = __fmul_rn(al, T);
-        const float2 gb = sC[k];
+        const float2 gb = lds_f2(aC + 8 * k);
         C0 = __fmaf_rn(q.w, w, C0);
         C1 = __fmaf_rn(gb.x, w, C1);
         C2 = __fmaf_rn(gb.y, w, C2);
