@@ -60,6 +60,7 @@ typedef struct gsc_ctx gsc_ctx;
 /* flags */
 #define GSC_F_DEPTH_LITERAL 0x1u /* SPEC-literal H(miss rate) instead of H(novelty) */
 #define GSC_F_STAGE_TIMING 0x2u  /* record CUDA events between the stages of every frame */
+#define GSC_F_DERIVE_CUDA_CORES 0x4u /* derivation MLP on CUDA cores (dp4a) instead of tcgen05 tensor cores */
 
 typedef struct {
   int width, height;        /* pixels per eye */

@@ -19,6 +19,7 @@ STATUS_NAMES = ["GSC_OK", "GSC_EINVAL", "GSC_EFORMAT", "GSC_EDEGENERATE", "GSC_E
                 "GSC_EINTERNAL", "GSC_ESTATE", "GSC_ECAPACITY"]
 GSC_F_DEPTH_LITERAL = 0x1
 GSC_F_STAGE_TIMING = 0x2
+GSC_F_DERIVE_CUDA_CORES = 0x4
 GSC_FMT_RGB_F32_PLANAR = 0
 GSC_FMT_RGBA8 = 1
 DBG = {"visible": 1, "misses": 2, "pool": 3, "splats": 4, "splat_g": 5, "pairs": 6, "pair_g": 7, "ranges": 8,

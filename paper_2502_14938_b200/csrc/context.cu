@@ -26,7 +26,7 @@ void launch_margin(int, const float *, const float *, const float *, float4 *, c
 int cull_tiles(int N);
 void launch_derive(const float pu[3], const uint32_t *, const float4 *, const int8_t *, const float *, const float *,
                    const int8_t *, const int32_t *, const int8_t *, const int32_t *, float *, float4 *,
-                   FrameCounters *, int, cudaStream_t);
+                   FrameCounters *, int, bool, cudaStream_t);
 void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, const SplatBufs &, uint32_t *,
                     FrameCounters *, int, cudaStream_t);
 int project_tile_size();
@@ -238,6 +238,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
     for (int k = 0; k < kF + 3; ++k) acc += 127 * (int64_t)std::abs((int)s->W1[k * 96 + n]);
     hmax = std::max(hmax, acc);
   }
+  if (hmax >= (1LL << 24)) return fail(ctx, GSC_EFORMAT, "hidden activations may exceed 24 bits (3 tensor-core limbs)");
   std::vector<int8_t> W1T(96 * 36, 0), W2T(kNOut * 32, 0);
   std::vector<int32_t> b1s(96), b2s(kNOut);
   for (int n = 0; n < 96; ++n) {
@@ -420,7 +421,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   mark();
   // a3
   launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p, ctx->b1s.p,
-                ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, st);
+                ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms,
+                (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, st);
   mark();
   // a4
   SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,

@@ -42,6 +42,17 @@ def test_c1_all_poses(orc, c1):
         assert d == 0.0
 
 
+def test_c1_derive_on_cuda_cores(orc, c1):
+    """The dp4a (CUDA-core) derivation path gives the same bits as the tcgen05 default."""
+    from paper_2502_14938_b200 import _abi
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg, flags=_abi.GSC_F_DERIVE_CUDA_CORES).load(sc)
+    for rig in sg.trajectory(cfg):
+        st, d = _frame_parity(orc, o, r, rig)
+        assert d == 0.0
+
+
 def test_c1_brute_force_pixels(orc, c1):
     """GPU pixels equal the oracle's per-pixel brute-force (O1) renderer."""
     cfg, sc = c1
