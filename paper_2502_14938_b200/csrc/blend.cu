@@ -1,17 +1,18 @@
 // blend.cu -- SURVEY §8(a) row a8: per-tile front-to-back alpha compositing
 // for both eyes (Eq. 1; Alg. 1; reading R17).
 //
-// One 256-thread CTA per (eye, 16x16 tile), one pixel per thread; warp w owns
-// the 16x2 pixel strip of rows 2w, 2w+1.  The tile's depth-sorted splats are
-// staged through shared memory in batches of 256 (40 bytes each); while
-// staging, each thread also computes an 8-bit strip mask: bit w is set unless
-// the padded bounding box of {power >= skip bound} misses strip w.  A warp
-// then walks only the batch entries of its strip (ballot + ffs), stops as
-// soon as all its 32 pixels have terminated, and the CTA leaves when all 256
-// have (__syncthreads_count).  Skipping a (pixel, splat) this way never
-// changes a decision: outside that box power < -ln(255 alpha) - 2^-7, so
-// alpha' < 1/255 (N5).  Per evaluated (pixel, splat), the exact op
-// order of DESIGN.md N6 (identical in the oracle):
+// One 256-thread CTA per (eye, 16x16 tile); warp w owns the 16x2 pixel strip
+// of rows 2w, 2w+1, one pixel per lane, and runs independently of the other
+// warps (no block barrier): it walks the tile's depth-sorted pair list in
+// chunks of 32, each lane fetching one splat record (the 8 warps of a CTA hit
+// the same records, so 7 of 8 fetches are L1 hits), keeps the splats whose
+// padded bounding box of {power >= skip bound} touches the strip (ballot),
+// stages those records in the warp's SMEM slots, evaluates them in depth order
+// and leaves as soon as all 32 of its pixels have terminated.  Skipping a
+// (pixel, splat) by the box never changes a decision: outside it
+// power < -ln(255 alpha) - 2^-7, so alpha' < 1/255 (N5).
+// Per evaluated (pixel, splat), the exact op order of DESIGN.md N6
+// (identical in the oracle):
 //   power  = fma(dx, fma(a', dx, b' dy), (c' dy) dy)      (skip if > 0)
 //   alpha' = min(0.99, alpha exp_s(power))                (skip if < 1/255)
 //   T' = fma(-alpha', T, T); stop before T' < 1e-4; C = fma(c, alpha' T, C)
@@ -20,8 +21,8 @@
 namespace gsc {
 
 constexpr int kBThreads = 256;
+constexpr int kBWarps = kBThreads / 32;
 
-// explicit 32-bit shared-window loads (keeps the window base out of the hot loop)
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -32,21 +33,14 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
-__device__ __forceinline__ uint32_t lds_u16(uint32_t a) {
-  unsigned short v;
-  asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
-  return v;
-}
 
 __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
-  __shared__ float4 sA[kBThreads];
-  __shared__ float4 sB[kBThreads];
-  __shared__ float2 sC[kBThreads];
-  __shared__ uint32_t sM[kBThreads];
-  __shared__ uint16_t sL[kBThreads / 32][kBThreads];
+  __shared__ float4 sA[kBWarps][32];
+  __shared__ float4 sB[kBWarps][32];
+  __shared__ float2 sC[kBWarps][32];
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
@@ -56,54 +50,44 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const int px = tx * kTile + (t & 15), py = ty * kTile + (t >> 4);
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
+  // this warp's strip: pixel centres x in [X0, X1], y in [Y0, Y0 + 1]
   const float X0 = __fadd_rn((float)(tx * kTile), 0.5f), X1 = __fadd_rn(X0, 15.0f);
-  const float Yb = __fadd_rn((float)(ty * kTile), 0.5f);
+  const float Y0 = __fadd_rn((float)(ty * kTile + 2 * (int)warp), 0.5f), Y1 = __fadd_rn(Y0, 1.0f);
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int done = !inside;
   uint32_t nev = 0, nexp = 0;
-  for (uint32_t b = rg.x; b < rg.y; b += kBThreads) {
-    __syncthreads();
-    const uint32_t idx = b + t;
+  uint32_t aA = (uint32_t)__cvta_generic_to_shared(&sA[warp][0]);
+  uint32_t aB = (uint32_t)__cvta_generic_to_shared(&sB[warp][0]);
+  uint32_t aC = (uint32_t)__cvta_generic_to_shared(&sC[warp][0]);
+  asm volatile("" : "+r"(aA), "+r"(aB), "+r"(aC));   // keep the slot addresses in registers
+  const uint32_t lt = lanemask_lt();
+
+  for (uint32_t b = rg.x; b < rg.y; b += 32) {
+    if (__all_sync(0xFFFFFFFFu, done)) break;
+    const uint32_t idx = b + lane;
+    bool in = false;
+    uint32_t c = 0;
+    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), cc = a;
     if (idx < rg.y) {
-      const uint32_t c = pair_vals[idx];
-      const float4 a = spA[c];
-      const float4 cc = spC[c];
-      sA[t] = a;
-      sB[t] = spB[c];
-      sC[t] = make_float2(cc.x, cc.y);
-      uint32_t mask = 0;
-      if (__fadd_rn(a.x, cc.z) >= X0 && __fsub_rn(a.x, cc.z) <= X1) {
-        const float lo = __fsub_rn(a.y, cc.w), hi = __fadd_rn(a.y, cc.w);
-#pragma unroll
-        for (int w = 0; w < 8; ++w) {
-          const float y0 = __fadd_rn(Yb, (float)(2 * w));
-          if (hi >= y0 && lo <= __fadd_rn(y0, 1.0f)) mask |= 1u << w;
-        }
-      }
-      sM[t] = mask;
+      c = pair_vals[idx];
+      a = spA[c];
+      cc = spC[c];
+      in = __fadd_rn(a.x, cc.z) >= X0 && __fsub_rn(a.x, cc.z) <= X1 && __fadd_rn(a.y, cc.w) >= Y0 &&
+           __fsub_rn(a.y, cc.w) <= Y1;
     }
-    __syncthreads();
-    const int cnt = min((uint32_t)kBThreads, rg.y - b);
-    if (!__all_sync(0xFFFFFFFFu, done)) {
-      // this warp's strip list (batch indices in depth order)
-      int n = 0;
-      for (int c0 = 0; c0 < cnt; c0 += 32) {
-        const bool in = c0 + (int)lane < cnt && ((sM[c0 + lane] >> warp) & 1u);
-        const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
-        if (in) sL[warp][n + __popc(bits & lanemask_lt())] = (uint16_t)(c0 + lane);
-        n += __popc(bits);
-      }
-      __syncwarp();
-      uint32_t aA = (uint32_t)__cvta_generic_to_shared(sA), aB = (uint32_t)__cvta_generic_to_shared(sB);
-      uint32_t aC = (uint32_t)__cvta_generic_to_shared(sC);
-      uint32_t aL = (uint32_t)__cvta_generic_to_shared(&sL[warp][0]);
-      // opaque to the compiler: keeps the addresses in registers instead of re-deriving the window base
-      asm volatile("" : "+r"(aA), "+r"(aB), "+r"(aC), "+r"(aL));
-      for (int i = 0; i < n; ++i) {
-        if ((i & 7) == 0 && __all_sync(0xFFFFFFFFu, done)) break;
-        if (done) continue;
-        const uint32_t k = lds_u16(aL + 2 * i);
+    // compact the strip's splats into the warp's slots, depth order preserved
+    const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
+    if (in) {
+      const uint32_t slot = __popc(bits & lt);
+      sA[warp][slot] = a;
+      sB[warp][slot] = spB[c];
+      sC[warp][slot] = make_float2(cc.x, cc.y);
+    }
+    const int n = __popc(bits);
+    __syncwarp();
+    if (!done) {
+      for (int k = 0; k < n; ++k) {
         ++nev;
         const float4 a = lds_f4(aA + 16 * k);     // (u, v, a' = -A/2, b' = -B)
         const float4 q = lds_f4(aB + 16 * k);     // (c' = -C/2, skip bound, alpha, r)
@@ -115,7 +99,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
         const float al = fminf(0.99f, __fmul_rn(q.z, exp_core(power)));   // power in [-5.6, 0]
         if (al < kAlphaMin) continue;
         const float Tn = __fmaf_rn(-al, T, T);
-        if (Tn < 0.0001f) { done = 1; continue; }
+        if (Tn < 0.0001f) { done = 1; break; }
         const float w = __fmul_rn(al, T);
         const float2 gb = lds_f2(aC + 8 * k);
         C0 = __fmaf_rn(q.w, w, C0);
@@ -124,7 +108,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
         T = Tn;
       }
     }
-    if (__syncthreads_count(done) == kBThreads) break;
+    __syncwarp();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
