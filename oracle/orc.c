@@ -426,8 +426,39 @@ float orc_tile_qmin(const orc_config *cfg, const orc_splat *s, int tx, int ty) {
   return q;
 }
 
+/* R14 (N7): row form of the exact tile test.  For tile row ty the ellipse
+ * {q <= thr} meets the band of pixel-centre rows [Y0, Y1] in the x-interval
+ * [xl, xr] (extremes of the ellipse's x-extent over the band; the extremes of
+ * x over the ellipse lie at dy = -/+ B sqrt(thr / (det C)), clamped to the
+ * band).  A tile is kept iff its pixel-centre column range [X0, X1] meets
+ * [xl, xr] -- in exact arithmetic the same set as q_min(tile) <= thr. */
+int orc_row_interval(const orc_config *cfg, const orc_splat *s, int ty, float *xl, float *xr) {
+  float det = (s->A * s->C) - (s->B * s->B);
+  float ey = sqrtf(s->thr * (s->A / det));
+  float sd = sqrtf(s->thr / (det * s->C));
+  int py1 = 16 * ty + 15;
+  if (py1 > cfg->height - 1) py1 = cfg->height - 1;
+  float Y0 = (float)(16 * ty) + 0.5f, Y1 = (float)py1 + 0.5f;
+  float lo = fmaxf(Y0 - s->v, -ey), hi = fminf(Y1 - s->v, ey);
+  if (!(lo <= hi)) return 0;
+  float bs = s->B * sd;
+  float at = s->A * s->thr;
+  float dyr = fminf(fmaxf(-bs, lo), hi);
+  float Dr = fmaxf(at - (det * (dyr * dyr)), 0.0f);
+  *xr = s->u + ((sqrtf(Dr) - (s->B * dyr)) / s->A);
+  float dyl = fminf(fmaxf(bs, lo), hi);
+  float Dl = fmaxf(at - (det * (dyl * dyl)), 0.0f);
+  *xl = s->u - ((sqrtf(Dl) + (s->B * dyl)) / s->A);
+  return 1;
+}
+
 int orc_tile_kept(const orc_config *cfg, const orc_splat *s, int tx, int ty) {
-  return orc_tile_qmin(cfg, s, tx, ty) <= s->thr;
+  float xl, xr;
+  if (!orc_row_interval(cfg, s, ty, &xl, &xr)) return 0;
+  int px1 = 16 * tx + 15;
+  if (px1 > cfg->width - 1) px1 = cfg->width - 1;
+  float X0 = (float)(16 * tx) + 0.5f, X1 = (float)px1 + 0.5f;
+  return X0 <= xr && X1 >= xl;
 }
 
 /* ======================================================================

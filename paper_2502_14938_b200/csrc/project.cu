@@ -18,7 +18,7 @@
 namespace gsc {
 
 constexpr int kPThreads = 256;
-constexpr int kPItems = 2;
+constexpr int kPItems = 1;
 constexpr int kPTile = 32 * kPItems;   // slots per warp tile
 
 struct SplatOut {
@@ -240,15 +240,136 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__r
   }
 }
 
-// Exact tile test of every candidate tile of every compacted splat
-// (warp-flattened over 32 splats at a time) -> kept count and the kept-tile
-// list (row-major keys eye*T_e + ty*TW + tx).  No ordering constraint: each
-// warp bump-allocates its list space.
+// ---- row form of the exact tile test (R14 / N7), one row of one splat per item
+struct WarpRows {
+  float u[32], v[32], A[32], B[32], thr[32], det[32], ey[32], bs[32];
+  int tx0[32], tx1[32], ty0[32];
+  uint32_t excl[32], cnt[32], kb[32];
+};
+
+// x-interval [xl, xr] of the ellipse {q <= thr} over the pixel-centre rows of tile row ty
+__device__ __forceinline__ bool row_interval(const WarpRows &ws, int o, int ty, int height, float &xl, float &xr) {
+  const float A = ws.A[o], B = ws.B[o], det = ws.det[o], ey = ws.ey[o], bs = ws.bs[o], v = ws.v[o], u = ws.u[o];
+  const int py1 = min(16 * ty + 15, height - 1);
+  const float Y0 = __fadd_rn((float)(16 * ty), 0.5f), Y1 = __fadd_rn((float)py1, 0.5f);
+  const float lo = fmaxf(__fsub_rn(Y0, v), -ey), hi = fminf(__fsub_rn(Y1, v), ey);
+  if (!(lo <= hi)) return false;
+  const float at = __fmul_rn(A, ws.thr[o]);
+  const float dyr = fminf(fmaxf(-bs, lo), hi);
+  const float Dr = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyr, dyr))), 0.0f);
+  xr = __fadd_rn(u, __fdiv_rn(__fsub_rn(__fsqrt_rn(Dr), __fmul_rn(B, dyr)), A));
+  const float dyl = fminf(fmaxf(bs, lo), hi);
+  const float Dl = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyl, dyl))), 0.0f);
+  xl = __fsub_rn(u, __fdiv_rn(__fadd_rn(__fsqrt_rn(Dl), __fmul_rn(B, dyl)), A));
+  return true;
+}
+
+// kept columns of row ty inside the candidate box [tx0, tx1]: X0(tx) <= xr and X1(tx) >= xl
+__device__ __forceinline__ void row_cols(float xl, float xr, int tx0, int tx1, int width, int &a, int &b) {
+  auto X0 = [](int tx) { return __fadd_rn((float)(16 * tx), 0.5f); };
+  auto X1 = [width](int tx) { return __fadd_rn((float)min(16 * tx + 15, width - 1), 0.5f); };
+  float fa = ceilf(__fmul_rn(__fsub_rn(xl, 15.5f), 0.0625f));
+  float fb = floorf(__fmul_rn(__fsub_rn(xr, 0.5f), 0.0625f));
+  a = (int)fminf(fmaxf(fa, (float)tx0), (float)tx1 + 1.0f);
+  b = (int)fminf(fmaxf(fb, (float)tx0 - 1.0f), (float)tx1);
+  while (a > tx0 && X1(a - 1) >= xl) --a;         // exact predicate decides at the edges
+  while (a <= tx1 && X1(a) < xl) ++a;
+  while (b < tx1 && X0(b + 1) <= xr) ++b;
+  while (b >= tx0 && X0(b) > xr) --b;
+}
+
+// Rows of the 32 lanes' candidate boxes walked as one list; each row's kept
+// columns are appended to the kept-tile list (row-major per splat, splats in
+// lane order) at positions from a warp scan of the row counts.
+__device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, uint32_t kb,
+                                                   int width, int height, int TW, uint32_t *list, uint32_t list_cap,
+                                                   uint32_t *list_top, uint32_t *overflow, uint32_t &list_off) {
+  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  const int tx0 = (int)(o.box_x & 0xFFFFu), tx1 = (int)(o.box_x >> 16);
+  const int ty0 = (int)(o.box_y & 0xFFFFu), ty1 = (int)((o.box_y >> 16) & 0x7FFFu);
+  const uint32_t nrows = has ? (uint32_t)(ty1 - ty0 + 1) : 0u;
+  const uint32_t area = has ? nrows * (uint32_t)(tx1 - tx0 + 1) : 0u;
+  uint32_t inc = nrows, tot_area = area;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+    if (lane >= (uint32_t)off) inc += t;
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) tot_area += __shfl_xor_sync(0xFFFFFFFFu, tot_area, off);
+  const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
+  ws.excl[lane] = inc - nrows;
+  ws.cnt[lane] = 0;
+  ws.kb[lane] = kb;
+  if (has) {
+    const float det = __fsub_rn(__fmul_rn(o.A, o.C), __fmul_rn(o.B, o.B));
+    ws.u[lane] = o.u; ws.v[lane] = o.v; ws.A[lane] = o.A; ws.B[lane] = o.B; ws.thr[lane] = o.thr;
+    ws.det[lane] = det;
+    ws.ey[lane] = __fsqrt_rn(__fmul_rn(o.thr, __fdiv_rn(o.A, det)));
+    ws.bs[lane] = __fmul_rn(o.B, __fsqrt_rn(__fdiv_rn(o.thr, __fmul_rn(det, o.C))));
+  }
+  ws.tx0[lane] = tx0; ws.tx1[lane] = tx1; ws.ty0[lane] = ty0;
+  __syncwarp();
+  uint32_t base = 0;
+  if (lane == 0) {
+    base = atomicAdd(list_top, tot_area);                   // upper bound: the boxes' areas
+    if (base + tot_area > list_cap || base + tot_area < base) atomicExch(overflow, 1u);
+  }
+  base = __shfl_sync(0xFFFFFFFFu, base, 0);
+  uint32_t run = base;
+  for (uint32_t w0 = 0; w0 < total; w0 += 32) {
+    const uint32_t w = w0 + lane;
+    int owner = 0, a = 0, b = -1, ty = 0;
+    if (w < total) {
+      int lo = 0;
+#pragma unroll
+      for (int step = 16; step > 0; step >>= 1)
+        if (ws.excl[lo + step] <= w) lo += step;
+      owner = lo;
+      ty = ws.ty0[lo] + (int)(w - ws.excl[lo]);
+      float xl, xr;
+      if (row_interval(ws, lo, ty, height, xl, xr)) row_cols(xl, xr, ws.tx0[lo], ws.tx1[lo], width, a, b);
+    }
+    const uint32_t n = b >= a ? (uint32_t)(b - a + 1) : 0u;
+    uint32_t ex = n;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ex, off);
+      if (lane >= (uint32_t)off) ex += t;
+    }
+    const uint32_t step_tot = __shfl_sync(0xFFFFFFFFu, ex, 31);
+    if (n) {
+      atomicAdd(&ws.cnt[owner], n);
+      const uint32_t key0 = ws.kb[owner] + (uint32_t)(ty * TW);
+      uint32_t pos = run + ex - n;
+      for (int tx = a; tx <= b; ++tx, ++pos)
+        if (pos < list_cap) list[pos] = key0 + (uint32_t)tx;
+    }
+    run += step_tot;
+  }
+  (void)lt;
+  __syncwarp();
+  const uint32_t n = has ? ws.cnt[lane] : 0u;
+  __syncwarp();
+  uint32_t e2 = n;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, e2, off);
+    if (lane >= (uint32_t)off) e2 += t;
+  }
+  list_off = base + e2 - n;
+  return n;
+}
+
+// Kept tiles of every compacted splat (rows of the 32 lanes' boxes walked as
+// one list) -> kept count and the kept-tile list (row-major keys
+// eye*T_e + ty*TW + tx).  No ordering constraint between warps: each warp
+// bump-allocates its list space.
 __global__ void __launch_bounds__(kPThreads)
 tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
-  __shared__ WarpTiles s_wt[kPThreads / 32];
+  __shared__ WarpRows s_wt[kPThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  WarpTiles &ws = s_wt[warp];
+  WarpRows &ws = s_wt[warp];
   const uint32_t C = ctr->n_splat;
   const uint32_t nw = (gridDim.x * kPThreads) >> 5;
   uint32_t pairs_local = 0;
@@ -267,8 +388,8 @@ tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
       kb = (bx.y >> 31) ? (uint32_t)fc.Te : 0u;
     }
     uint32_t loff = 0;
-    const uint32_t n = warp_count_list(ws, has, o, kb, fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
-                                       &ctr->list_top, &ctr->overflow, loff);
+    const uint32_t n = warp_rows_list(ws, has, o, kb, fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
+                                      &ctr->list_top, &ctr->overflow, loff);
     if (in) {
       sb.count[c] = n;
       sb.list_off[c] = loff;

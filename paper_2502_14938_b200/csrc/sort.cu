@@ -39,7 +39,7 @@ struct SortSmem {
 };
 
 template <bool kIota>
-__global__ void __launch_bounds__(kSThreads)
+__global__ void __launch_bounds__(kSThreads, 4)
 onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                      uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
                      const uint32_t *__restrict__ d_count, uint32_t shift, const uint32_t *__restrict__ hist,
@@ -113,13 +113,23 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
         st_volatile_u32(st, (2u << 30) | run);
       } else {
         st_volatile_u32(st, (1u << 30) | run);
+        // look back 8 predecessor tiles per step with the 8 loads in flight together
+        // (the inclusive frontier lags the aggregates in the first wave of tiles)
         int64_t p = (int64_t)tile - 1;
-        while (p >= 0) {
-          uint32_t s;
-          do { s = ld_volatile_u32(status + (size_t)p * kBins + d); } while ((s >> 30) == 0);
-          pre += s & 0x3FFFFFFFu;
-          if ((s >> 30) == 2u) break;
-          --p;
+        bool found = false;
+        while (!found) {
+          uint32_t s[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            s[j] = (p - j >= 0) ? ld_volatile_u32(status + (size_t)(p - j) * kBins + d) : (2u << 30);
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            if (found) break;
+            while ((s[j] >> 30) == 0) s[j] = ld_volatile_u32(status + (size_t)(p - j) * kBins + d);
+            pre += s[j] & 0x3FFFFFFFu;
+            found = (s[j] >> 30) == 2u;
+          }
+          p -= 8;
         }
         st_volatile_u32(st, (2u << 30) | (pre + run));
       }
