@@ -127,6 +127,22 @@ def test_elementary_functions_bitwise(orc, fn, lo, hi, step):
     assert nbad == 0
 
 
+def test_rgba8_output_matches_f32(orc, c1):
+    """The display format bench.py times (RGBA8) is the f32 result quantised:
+    round(255 clamp(x)) per channel, alpha = round(255 (1 - T))."""
+    import torch
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    rig = sg.trajectory(cfg)[1]
+    r1 = renderer(cfg).load(sc)
+    fl, fr, _ = r1.render(rig)
+    r2 = renderer(cfg).load(sc)
+    ql, qr, _ = r2.render(rig, fmt=gp.GSC_FMT_RGBA8)
+    for f, q in ((fl, ql), (fr, qr)):
+        want = torch.clamp(torch.round(f.permute(1, 2, 0) * 255.0), 0, 255).to(torch.uint8)
+        assert torch.equal(q[..., :3], want)
+
+
 # ---------------------------------------------------------------- configs[1..2] (100k, 2K binocular)
 @pytest.fixture(scope="module")
 def c100k():
@@ -159,3 +175,28 @@ def test_c3_trajectory_reuse(orc, c100k):
         st, d = _frame_parity(orc, o, r, rig, full=f in (0, 1, 150, 299))
         hits += st["n_hits"]
     assert hits > 0
+
+
+# ---------------------------------------------------------------- configs[3] at full size (bench launch config)
+@pytest.fixture(scope="module")
+def c4():
+    cfg = sg.config("C4")
+    return cfg, cfg.scene()
+
+
+def test_c4_full_size_bench_config(orc, c4):
+    """configs[3] (1M anchors, 2K binocular) in the launch configuration
+    bench.py times (stage timing on, default capacities): frame 0 (cold cache,
+    633k misses) and frame 30 (after 29 cached frames) fully bit-exact -- sets,
+    pool, splat records, 30M+ sorted keys, pixels -- and the hit/miss sets of
+    every frame in between."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c4
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg, flags=gp.GSC_F_STAGE_TIMING).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(31):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in (0, 30))
+        assert not st["overflow"]
+        if f in (0, 30):
+            assert d == 0.0
