@@ -113,7 +113,12 @@ def run_gsc(args):
     import paper_2502_14938_b200 as gp
     from paper_2502_14938_b200 import multi
 
-    rank, world, local = multi.init()
+    # GSC_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo process group -- exercises the
+    # multi-rank path on a 1-GPU box (timings then share one GPU and are not a scaling result)
+    share = os.environ.get("GSC_BENCH_SHARE_GPU") == "1"
+    rank, world, local = multi.init(backend="gloo" if share else None)
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     cfg = sg.config(args.config)
@@ -147,7 +152,7 @@ def run_gsc(args):
     multi.barrier()
     clocks = sampler.stop()
     t_ms = e0.elapsed_time(e1)
-    t_max = multi.max_over_ranks(t_ms, dev)
+    t_max = multi.max_over_ranks(t_ms, None if share else dev)
     hist = r.stats_history(max(args.steps, 1))
     overflow = any(h["overflow"] for h in hist)
 
@@ -161,7 +166,7 @@ def run_gsc(args):
         r.render_host(traj[f], hl, hr, fmt)
     t1 = time.perf_counter()
     multi.barrier()
-    e2e_max = multi.max_over_ranks(t1 - t0, dev)
+    e2e_max = multi.max_over_ranks(t1 - t0, None if share else dev)
 
     total_frames = world * len(frames)
     value = total_frames / (t_max / 1000.0) if t_max > 0 else 0.0
