@@ -96,14 +96,20 @@ def _stage_bytes(s, N, K, W, H, fmt_bytes):
     """Algorithmic HBM bytes per stage for one frame."""
     V, M, C, P = s["n_visible"], s["n_misses"], s["n_splats"], s["n_pairs"]
     return {
+        # pos_m 16 + level 1 + birth 4 per anchor, bitsets, ids out, birth writes
         "cull": N * (16 + 1 + 4) + N / 4.0 + 4 * V + 8 * M,
+        # miss id, pos, feat, offs, scale in; alpha + 48-byte pool record out per slot
         "derive": M * (4 + 16 + 32 + 120 + 12) + M * K * (4 + 48),
-        "project": 4 * V + 4 * V * K + 48 * (C / 2.0) + C * (16 * 3 + 8 + 4 * 3),
+        # project: ids, alpha per slot, pool per live slot (C/2), 72-byte record per splat;
+        # tiles: 36 B read + 8 B written per splat, 4 B per kept tile
+        "project": 4 * V + 4 * V * K + 48 * (C / 2.0) + 72 * C + 44 * C + 4 * P,
         "depth_sort": 12 * C + 3 * 16 * C,
-        "emit": C * (4 + 4 + 16 + 4 + 16 + 8) + 8 * P,
+        # pairoff 12 B per splat; expand 12 B per pair + 12 B per splat
+        "emit": 24 * C + 12 * P,
         "tile_sort": 2 * 16 * P,
         "ranges": 4 * P,
-        "blend": 4 * P + 36 * P + 2 * W * H * fmt_bytes,
+        # pair value + 48-byte record per pair, output images
+        "blend": 52 * P + 2 * W * H * fmt_bytes,
     }
 
 
@@ -199,6 +205,19 @@ def run_gsc(args):
         roof = {"kernel": dom, "bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
                 "note": f"algorithmic bytes/frame {algo[dom] / nf:.4g}; peak {peaks['src']}"}
+    # DRAM traffic of the dominant kernel from the committed ncu --set full capture
+    kernels = {"blend": ["blend_kernel"], "project": ["project_kernel", "tiles_kernel"], "cull": ["cull_classify_kernel"],
+               "derive": ["derive_mma_kernel"], "depth_sort": ["onesweep_pass_kernel"] * 4,
+               "tile_sort": ["onesweep_pass_kernel"] * 2, "emit": ["pairoff_kernel", "expand_kernel"],
+               "ranges": ["ranges_kernel"]}
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            tr = json.load(fh)
+        roof["traffic"] = sum(tr[k]["dram_bytes_per_launch"] for k in kernels[dom])
+        roof["traffic_unit"] = "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)"
+        roof["traffic_source"] = tr[kernels[dom][0]]["source"]
+    except (OSError, KeyError, ValueError):
+        pass
     stage_report = {s: {"ms_per_frame": round(ms[s] / nf, 4),
                         "GBps": round(algo[s] / (ms[s] / 1000.0) / 1e9, 1) if ms[s] > 0 else None}
                     for s in stages}
