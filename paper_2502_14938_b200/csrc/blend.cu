@@ -38,29 +38,30 @@ __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
-  __shared__ float4 sA[kBWarps][32];
-  __shared__ float4 sB[kBWarps][32];
-  __shared__ float2 sC[kBWarps][32];
+  // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
+  // walks all three (offsets 0, 512, 1024 bytes)
+  __shared__ float4 slots[kBWarps][96];
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
   const int e = tile >= fc.Te;
   const int tl = tile - e * fc.Te;
   const int tx = tl % fc.TW, ty = tl / fc.TW;
-  const int px = tx * kTile + (t & 15), py = ty * kTile + (t >> 4);
+  // warp w owns the 8x4 block of columns 8 (w & 1) .. +7, rows 4 (w >> 1) .. +3 (squarer than 16x2:
+  // fewer blocks per small splat)
+  const int bx0 = tx * kTile + 8 * (int)(warp & 1), by0 = ty * kTile + 4 * (int)(warp >> 1);
+  const int px = bx0 + (int)(lane & 7), py = by0 + (int)(lane >> 3);
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
-  // this warp's strip: pixel centres x in [X0, X1], y in [Y0, Y0 + 1]
-  const float X0 = __fadd_rn((float)(tx * kTile), 0.5f), X1 = __fadd_rn(X0, 15.0f);
-  const float Y0 = __fadd_rn((float)(ty * kTile + 2 * (int)warp), 0.5f), Y1 = __fadd_rn(Y0, 1.0f);
+  // this warp's block: pixel centres x in [X0, X1], y in [Y0, Y1]
+  const float X0 = __fadd_rn((float)bx0, 0.5f), X1 = __fadd_rn(X0, 7.0f);
+  const float Y0 = __fadd_rn((float)by0, 0.5f), Y1 = __fadd_rn(Y0, 3.0f);
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   int done = !inside;
   uint32_t nev = 0, nexp = 0;
-  uint32_t aA = (uint32_t)__cvta_generic_to_shared(&sA[warp][0]);
-  uint32_t aB = (uint32_t)__cvta_generic_to_shared(&sB[warp][0]);
-  uint32_t aC = (uint32_t)__cvta_generic_to_shared(&sC[warp][0]);
-  asm volatile("" : "+r"(aA), "+r"(aB), "+r"(aC));   // keep the slot addresses in registers
+  uint32_t base = (uint32_t)__cvta_generic_to_shared(&slots[warp][0]);
+  asm volatile("" : "+r"(base));   // keep the slot address in a register
   const uint32_t lt = lanemask_lt();
 
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
@@ -80,17 +81,18 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
     if (in) {
       const uint32_t slot = __popc(bits & lt);
-      sA[warp][slot] = a;
-      sB[warp][slot] = spB[c];
-      sC[warp][slot] = make_float2(cc.x, cc.y);
+      slots[warp][slot] = a;
+      slots[warp][32 + slot] = spB[c];
+      slots[warp][64 + slot] = cc;
     }
-    const int n = __popc(bits);
+    const uint32_t n = __popc(bits);
     __syncwarp();
     if (!done) {
-      for (int k = 0; k < n; ++k) {
-        ++nev;
-        const float4 a = lds_f4(aA + 16 * k);     // (u, v, a' = -A/2, b' = -B)
-        const float4 q = lds_f4(aB + 16 * k);     // (c' = -C/2, skip bound, alpha, r)
+      nev += n;   // minus the ones after a termination, below
+      uint32_t end = base + 16 * n;
+      for (uint32_t p = base; p < end; p += 16) {
+        const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
+        const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
         const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
@@ -99,13 +101,18 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
         const float al = fminf(0.99f, __fmul_rn(q.z, exp_core(power)));   // power in [-5.6, 0]
         if (al < kAlphaMin) continue;
         const float Tn = __fmaf_rn(-al, T, T);
-        if (Tn < 0.0001f) { done = 1; break; }
-        const float w = __fmul_rn(al, T);
-        const float2 gb = lds_f2(aC + 8 * k);
-        C0 = __fmaf_rn(q.w, w, C0);
-        C1 = __fmaf_rn(gb.x, w, C1);
-        C2 = __fmaf_rn(gb.y, w, C2);
-        T = Tn;
+        if (Tn < 0.0001f) {   // terminate: the remaining slots are not evaluated
+          done = 1;
+          nev -= (end - p) / 16 - 1;
+          end = p;
+        } else {
+          const float w = __fmul_rn(al, T);
+          const float2 gb = lds_f2(p + 1024);
+          C0 = __fmaf_rn(q.w, w, C0);
+          C1 = __fmaf_rn(gb.x, w, C1);
+          C2 = __fmaf_rn(gb.y, w, C2);
+          T = Tn;
+        }
       }
     }
     __syncwarp();
