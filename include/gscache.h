@@ -61,6 +61,8 @@ typedef struct gsc_ctx gsc_ctx;
 #define GSC_F_DEPTH_LITERAL 0x1u /* SPEC-literal H(miss rate) instead of H(novelty) */
 #define GSC_F_STAGE_TIMING 0x2u  /* record CUDA events between the stages of every frame */
 #define GSC_F_DERIVE_CUDA_CORES 0x4u /* derivation MLP on CUDA cores (dp4a) instead of tcgen05 tensor cores */
+#define GSC_F_COUNT_EVALS 0x8u   /* blend counts its evaluations (gsc_frame_stats.n_evals / n_exp; else 0);
+                                    costs blend time, so bench.py counts in a separate untimed pass */
 
 typedef struct {
   int width, height;        /* pixels per eye */
@@ -105,8 +107,8 @@ typedef struct {
   float update_rate, novelty_rate;               /* misses/|X_f|, new/|X_f| */
   /* stage times in ms (GSC_F_STAGE_TIMING; else 0): */
   float ms_cull, ms_derive, ms_project, ms_depth_sort, ms_emit, ms_tile_sort, ms_ranges, ms_blend, ms_total;
-  uint64_t n_evals;                              /* blend: (pixel, splat) evaluations executed */
-  uint64_t n_exp;                                /* blend: evaluations inside the skip bound (exp evaluated) */
+  uint64_t n_evals;                              /* blend: (pixel, splat) evaluations executed (GSC_F_COUNT_EVALS) */
+  uint64_t n_exp;                                /* blend: evaluations inside the skip bound (GSC_F_COUNT_EVALS) */
 } gsc_frame_stats;
 
 /* out formats */
@@ -166,13 +168,20 @@ gsc_status gsc_stats_history(gsc_ctx *ctx, gsc_frame_stats *dst, int max, int *n
 /* Drop every cache line and restart the frame counter at 0 (Alg. 1 "first frame"). */
 gsc_status gsc_reset_cache(gsc_ctx *ctx);
 
+/* Replace gsc_config.flags.  GSC_F_STAGE_TIMING, GSC_F_DERIVE_CUDA_CORES and
+ * GSC_F_COUNT_EVALS apply from the next frame; GSC_F_DEPTH_LITERAL from the
+ * next gsc_reset_cache (it selects the cache policy the state machine
+ * started with).  Synchronises the device.  GSC_EINVAL on unknown bits. */
+gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags);
+
 /* Copy an intermediate of the most recent frame to host memory (debug/parity).
  * *len_bytes receives the full size; at most capacity_bytes are written.
  * Synchronises the context's last stream. */
 gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t capacity_bytes, size_t *len_bytes);
 
 /* Evaluate the device elementary functions (0 exp_s, 1 log_s, 2 tanh_s,
- * 3 sigmoid_s; DESIGN.md Numerics) on n device floats (parity sweeps). */
+ * 3 sigmoid_s, 4 exp_blend = the blend's exp_s for x in [-87, 0];
+ * DESIGN.md Numerics) on n device floats (parity sweeps). */
 gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n);
 
 const char *gsc_last_error(const gsc_ctx *ctx);

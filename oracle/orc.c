@@ -41,8 +41,8 @@ float orc_exp_s(float x) {
   const float ln2_lo = 1.428606765330187045037746429443359375e-06f; /* 0x35BFBE8E */
   float t = x * log2e;
   float n = rintf(t);                                /* round half to even */
-  float r = x - n * ln2_hi;
-  r = r - n * ln2_lo;
+  float r = fmaf(-n, ln2_hi, x);                     /* exact (n ln2_hi has <= 24 bits) */
+  r = fmaf(-n, ln2_lo, r);                           /* one rounding */
   /* Taylor degree 7 (|r| <= 0.3466: truncation < 6e-9 relative), Horner with fmaf */
   float p = 1.98412698e-04f;                         /* 1/5040 */
   p = fmaf(p, r, 1.38888889e-03f);                   /* 1/720 */

@@ -10,11 +10,11 @@ from __future__ import annotations
 import math
 
 from . import _abi
-from ._abi import (GSC_F_DEPTH_LITERAL, GSC_F_STAGE_TIMING, GSC_FMT_RGB_F32_PLANAR, GSC_FMT_RGBA8, GscError,
-                   gsc_frame_stats)
+from ._abi import (GSC_F_COUNT_EVALS, GSC_F_DEPTH_LITERAL, GSC_F_DERIVE_CUDA_CORES, GSC_F_STAGE_TIMING,
+                   GSC_FMT_RGB_F32_PLANAR, GSC_FMT_RGBA8, GscError, gsc_frame_stats)
 
-__all__ = ["Renderer", "GscError", "GSC_F_DEPTH_LITERAL", "GSC_F_STAGE_TIMING", "GSC_FMT_RGB_F32_PLANAR",
-           "GSC_FMT_RGBA8", "build"]
+__all__ = ["Renderer", "GscError", "GSC_F_DEPTH_LITERAL", "GSC_F_STAGE_TIMING", "GSC_F_DERIVE_CUDA_CORES",
+           "GSC_F_COUNT_EVALS", "GSC_FMT_RGB_F32_PLANAR", "GSC_FMT_RGBA8", "build"]
 
 
 def build(force: bool = False) -> str:
@@ -76,6 +76,10 @@ class Renderer:
 
     def reset_cache(self):
         self._chk(_abi.lib().gsc_reset_cache(self.h))
+
+    def set_flags(self, flags: int):
+        """Replace the GSC_F_* flags (DEPTH_LITERAL takes effect at the next reset_cache)."""
+        self._chk(_abi.lib().gsc_set_flags(self.h, flags))
 
     # -- rendering
     def alloc_outputs(self, fmt: int = GSC_FMT_RGB_F32_PLANAR):
@@ -145,11 +149,12 @@ class Renderer:
         return out
 
     def elementary(self, fn: str, x):
-        """Evaluate a device elementary function (exp/log/tanh/sigmoid) on a CUDA float32 tensor."""
+        """Evaluate a device elementary function (exp/log/tanh/sigmoid, exp_blend = the blend's exp
+        for x in [-87, 0]) on a CUDA float32 tensor."""
         import ctypes as C
         import torch
         out = torch.empty_like(x)
-        code = {"exp": 0, "log": 1, "tanh": 2, "sigmoid": 3}[fn]
+        code = {"exp": 0, "log": 1, "tanh": 2, "sigmoid": 3, "exp_blend": 4}[fn]
         self._chk(_abi.lib().gsc_selftest_elementary(self.h, code, C.c_void_p(x.data_ptr()),
                                                      C.c_void_p(out.data_ptr()), x.numel()))
         return out

@@ -20,6 +20,7 @@ STATUS_NAMES = ["GSC_OK", "GSC_EINVAL", "GSC_EFORMAT", "GSC_EDEGENERATE", "GSC_E
 GSC_F_DEPTH_LITERAL = 0x1
 GSC_F_STAGE_TIMING = 0x2
 GSC_F_DERIVE_CUDA_CORES = 0x4
+GSC_F_COUNT_EVALS = 0x8
 GSC_FMT_RGB_F32_PLANAR = 0
 GSC_FMT_RGBA8 = 1
 DBG = {"visible": 1, "misses": 2, "pool": 3, "splats": 4, "splat_g": 5, "pairs": 6, "pair_g": 7, "ranges": 8,
@@ -76,6 +77,7 @@ _SIGS = {
     "gsc_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gsc_stats_history": (C.c_int, [C.c_void_p, C.POINTER(gsc_frame_stats), C.c_int, C.POINTER(C.c_int)]),
     "gsc_reset_cache": (C.c_int, [C.c_void_p]),
+    "gsc_set_flags": (C.c_int, [C.c_void_p, C.c_uint]),
     "gsc_debug_fetch": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     "gsc_selftest_elementary": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_size_t]),
     "gsc_last_error": (C.c_char_p, [C.c_void_p]),

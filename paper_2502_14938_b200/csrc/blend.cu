@@ -1,16 +1,21 @@
 // blend.cu -- SURVEY §8(a) row a8: per-tile front-to-back alpha compositing
 // for both eyes (Eq. 1; Alg. 1; reading R17).
 //
-// One 256-thread CTA per (eye, 16x16 tile); warp w owns the 16x2 pixel strip
-// of rows 2w, 2w+1, one pixel per lane, and runs independently of the other
-// warps (no block barrier): it walks the tile's depth-sorted pair list in
-// chunks of 32, each lane fetching one splat record (the 8 warps of a CTA hit
-// the same records, so 7 of 8 fetches are L1 hits), keeps the splats whose
-// padded bounding box of {power >= skip bound} touches the strip (ballot),
-// stages those records in the warp's SMEM slots, evaluates them in depth order
-// and leaves as soon as all 32 of its pixels have terminated.  Skipping a
-// (pixel, splat) by the box never changes a decision: outside it
-// power < -ln(255 alpha) - 2^-7, so alpha' < 1/255 (N5).
+// One 256-thread CTA per (eye, 16x16 tile); warp w owns the 8x4 pixel block
+// at columns 8 (w & 1) .., rows 4 (w >> 1) .., one pixel per lane, and runs
+// independently of the other warps (no block barrier): it walks the tile's
+// depth-sorted pair list in chunks of 32, each lane fetching one splat record
+// (the 8 warps of a CTA hit the same records, so 7 of 8 fetches are L1 hits),
+// keeps the splats whose padded bounding box of {power >= skip bound} touches
+// the block (ballot), stages those records in the warp's SMEM slots,
+// evaluates them in depth order and leaves as soon as all 32 of its pixels
+// have terminated.  Skipping a (pixel, splat) by the box never changes a
+// decision: outside it power < -ln(255 alpha) - 2^-7, so alpha' < 1/255
+// (N5).  The evaluation loop is warp-uniform (no divergent
+// branches): a lane that skips a splat, or has terminated, composites it with
+// alpha' = 0, which leaves T and C bit-identical (fma(-0, T, T) = T,
+// fma(c, 0, C) = C); only when no lane of the warp needs the exp is the splat
+// skipped outright.
 // Per evaluated (pixel, splat), the exact op order of DESIGN.md N6
 // (identical in the oracle):
 //   power  = fma(dx, fma(a', dx, b' dy), (c' dy) dy)      (skip if > 0)
@@ -34,6 +39,7 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
   return v;
 }
 
+template <bool kCount>   // kCount: accumulate n_evals / n_exp (GSC_F_COUNT_EVALS)
 __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
@@ -58,14 +64,17 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const float Y0 = __fadd_rn((float)by0, 0.5f), Y1 = __fadd_rn(Y0, 3.0f);
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  int done = !inside;
+  // a lane's liveness floor on power: -inf while it composites, +inf once it has terminated (or lies
+  // outside the image), so nothing is live for it any more (one FMNMX instead of a predicate chain)
+  const float kInf = __int_as_float(0x7F800000);
+  float pfloor = inside ? -kInf : kInf;
   uint32_t nev = 0, nexp = 0;
   uint32_t base = (uint32_t)__cvta_generic_to_shared(&slots[warp][0]);
   asm volatile("" : "+r"(base));   // keep the slot address in a register
   const uint32_t lt = lanemask_lt();
 
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
-    if (__all_sync(0xFFFFFFFFu, done)) break;
+    if (__all_sync(0xFFFFFFFFu, pfloor > 0.0f)) break;
     const uint32_t idx = b + lane;
     bool in = false;
     uint32_t c = 0;
@@ -87,44 +96,48 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     }
     const uint32_t n = __popc(bits);
     __syncwarp();
-    if (!done) {
-      nev += n;   // minus the ones after a termination, below
-      uint32_t end = base + 16 * n;
-      for (uint32_t p = base; p < end; p += 16) {
-        const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
-        const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
-        const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
-        const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
-        const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
-        if (power < q.y || power > 0.0f) continue;
-        ++nexp;
-        const float al = fminf(0.99f, __fmul_rn(q.z, exp_core(power)));   // power in [-5.6, 0]
-        if (al < kAlphaMin) continue;
-        const float Tn = __fmaf_rn(-al, T, T);
-        if (Tn < 0.0001f) {   // terminate: the remaining slots are not evaluated
-          done = 1;
-          nev -= (end - p) / 16 - 1;
-          end = p;
-        } else {
-          const float w = __fmul_rn(al, T);
-          const float2 gb = lds_f2(p + 1024);
-          C0 = __fmaf_rn(q.w, w, C0);
-          C1 = __fmaf_rn(gb.x, w, C1);
-          C2 = __fmaf_rn(gb.y, w, C2);
-          T = Tn;
-        }
+    const uint32_t end = base + 16 * n;
+    const bool done0 = pfloor > 0.0f;
+    uint32_t pstop = end;
+#pragma unroll 2
+    for (uint32_t p = base; p < end; p += 16) {   // warp-uniform trip count
+      const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
+      const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
+      const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
+      const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
+      const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
+      const bool live = power >= fmaxf(q.y, pfloor) && power <= 0.0f;
+      if (!__any_sync(0xFFFFFFFFu, live)) continue;
+      if (kCount) nexp += live;
+      float al = fminf(0.99f, __fmul_rn(q.z, exp_blend(power)));   // garbage (discarded) if !live
+      al = (al >= kAlphaMin) & live ? al : 0.0f;
+      const float Tn = __fmaf_rn(-al, T, T);
+      const bool term = Tn < 0.0001f;   // terminate before this splat; the rest is not evaluated
+      if (kCount && term) pstop = p;
+      if (!term) {
+        const float w = __fmul_rn(al, T);
+        const float2 gb = lds_f2(p + 1024);
+        C0 = __fmaf_rn(q.w, w, C0);
+        C1 = __fmaf_rn(gb.x, w, C1);
+        C2 = __fmaf_rn(gb.y, w, C2);
+        T = Tn;
       }
+      // pfloor = term ? inf : pfloor as one predicated move (the C form compiles to three)
+      asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, 0f38D1B717;\n @p mov.b32 %0, 0x7F800000;\n}" : "+f"(pfloor) : "f"(Tn));
     }
+    if (kCount && !done0) nev += (pstop - base) / 16 + (pfloor > 0.0f ? 1 : 0);
     __syncwarp();
   }
+  if (kCount) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
-    nexp += __shfl_xor_sync(0xFFFFFFFFu, nexp, o);
-  }
-  if (lane == 0 && nev) {
-    atomicAdd(&ctr->n_evals, (unsigned long long)nev);
-    atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
+    for (int o = 16; o > 0; o >>= 1) {
+      nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
+      nexp += __shfl_xor_sync(0xFFFFFFFFu, nexp, o);
+    }
+    if (lane == 0 && nev) {
+      atomicAdd(&ctr->n_evals, (unsigned long long)nev);
+      atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
+    }
   }
   if (!inside) return;
   const float o0 = __fmaf_rn(T, fc.bg[0], C0);
@@ -148,15 +161,18 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
 
 void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_vals, const float4 *spA,
                   const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, FrameCounters *ctr,
-                  cudaStream_t st) {
-  blend_kernel<<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+                  bool count, cudaStream_t st) {
+  if (count)
+    blend_kernel<true><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+  else
+    blend_kernel<false><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
 }
 
 // elementary-function self test (parity sweeps through the C ABI)
 __global__ void elem_kernel(int fn, const float *__restrict__ in, float *__restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     float x = in[i];
-    out[i] = fn == 0 ? exp_s(x) : fn == 1 ? log_s(x) : fn == 2 ? tanh_s(x) : sigmoid_s(x);
+    out[i] = fn == 0 ? exp_s(x) : fn == 1 ? log_s(x) : fn == 2 ? tanh_s(x) : fn == 3 ? sigmoid_s(x) : exp_blend(x);
   }
 }
 void launch_elem(int fn, const float *in, float *out, size_t n, int num_sms, cudaStream_t st) {

@@ -35,7 +35,7 @@ void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, cudaStream_t);
 void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const float4 *, const float4 *, const float4 *,
-                  void *, void *, int, FrameCounters *, cudaStream_t);
+                  void *, void *, int, FrameCounters *, bool, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 int sort_tile_size();
 int emit_tile_size();
@@ -448,7 +448,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   launch_ranges(ctx->pkey_a.p, ctr, ctx->ranges.p, ctx->num_sms, st);
   mark();
   // a8
-  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr, st);
+  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr,
+               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, st);
   launch_record(ctr, ctx->rec_dev.p + slot_i, st);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
                      st));
@@ -595,6 +596,16 @@ gsc_status gsc_reset_cache(gsc_ctx *ctx) {
   return reset_cache(ctx, nullptr);
 }
 
+gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
+  if (!ctx) return GSC_EINVAL;
+  const unsigned known = GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS;
+  if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
+  CU(cudaSetDevice(ctx->device));
+  CU(cudaDeviceSynchronize());
+  ctx->cfg.flags = flags;
+  return GSC_OK;
+}
+
 gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, size_t *len) {
   if (!ctx || !len) return GSC_EINVAL;
   CU(cudaSetDevice(ctx->device));
@@ -688,7 +699,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
 }
 
 gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n) {
-  if (!ctx || fn < 0 || fn > 3 || (n && (!dev_in || !dev_out))) return GSC_EINVAL;
+  if (!ctx || fn < 0 || fn > 4 || (n && (!dev_in || !dev_out))) return GSC_EINVAL;
   CU(cudaSetDevice(ctx->device));
   launch_elem(fn, dev_in, dev_out, n, ctx->num_sms, nullptr);
   CU(cudaGetLastError());

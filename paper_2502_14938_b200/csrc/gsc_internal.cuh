@@ -169,14 +169,19 @@ __device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *s
 // ---------------------------------------------------------------- elementary functions
 // DESIGN.md Numerics N1-N4.  Independent implementation of the same op
 // sequence the oracle uses; __fmaf_rn only where the definition says fma.
-// exp_s without the special-value branches; identical to exp_s on [-87.33654, 88.0]
-__device__ __forceinline__ float exp_core(float x) {
+// exp_s on [-87, 0] where the result is normal (the blend's power range), in 13 instructions:
+// s = t + 1.5 2^23 rounds t to the nearest integer n (ties to even, |t| < 2^22) and holds n in its low
+// mantissa bits, so bits(s) << 23 = n << 23 (mod 2^32); multiplying the polynomial by 2^n is then an
+// integer add into its exponent field, exact while the product is normal.  Same bits as exp_s there.
+__device__ __forceinline__ float exp_blend(float x) {
   const float log2e = 1.44269502162933349609375f;
   const float ln2_hi = 0.693145751953125f;
   const float ln2_lo = 1.428606765330187045037746429443359375e-06f;
-  float n = rintf(__fmul_rn(x, log2e));
-  float r = __fsub_rn(x, __fmul_rn(n, ln2_hi));
-  r = __fsub_rn(r, __fmul_rn(n, ln2_lo));
+  const float magic = 12582912.0f;   // 1.5 * 2^23
+  const float s = __fadd_rn(__fmul_rn(x, log2e), magic);
+  const float n = __fsub_rn(s, magic);
+  float r = __fmaf_rn(-n, ln2_hi, x);
+  r = __fmaf_rn(-n, ln2_lo, r);
   float p = 1.98412698e-04f;
   p = __fmaf_rn(p, r, 1.38888889e-03f);
   p = __fmaf_rn(p, r, 8.33333377e-03f);
@@ -185,7 +190,7 @@ __device__ __forceinline__ float exp_core(float x) {
   p = __fmaf_rn(p, r, 0.5f);
   p = __fmaf_rn(p, r, 1.0f);
   p = __fmaf_rn(p, r, 1.0f);
-  return __fmul_rn(p, __uint_as_float((uint32_t)(__float2int_rz(n) + 127) << 23));
+  return __uint_as_float(__float_as_uint(p) + (__float_as_uint(s) << 23));
 }
 
 __device__ __forceinline__ float exp_s(float x) {
@@ -196,8 +201,8 @@ __device__ __forceinline__ float exp_s(float x) {
   const float ln2_hi = 0.693145751953125f;
   const float ln2_lo = 1.428606765330187045037746429443359375e-06f;
   float n = rintf(__fmul_rn(x, log2e));
-  float r = __fsub_rn(x, __fmul_rn(n, ln2_hi));
-  r = __fsub_rn(r, __fmul_rn(n, ln2_lo));
+  float r = __fmaf_rn(-n, ln2_hi, x);
+  r = __fmaf_rn(-n, ln2_lo, r);
   float p = 1.98412698e-04f;
   p = __fmaf_rn(p, r, 1.38888889e-03f);
   p = __fmaf_rn(p, r, 8.33333377e-03f);

@@ -103,10 +103,12 @@ def test_reset_and_empty_frames(orc, c1):
 
 
 @pytest.mark.parametrize("fn,lo,hi,step", [("exp", -90.0, 90.0, 1), ("log", 1e-30, 1e30, 3),
-                                           ("tanh", -20.0, 20.0, 3), ("sigmoid", -90.0, 90.0, 3)])
+                                           ("tanh", -20.0, 20.0, 3), ("sigmoid", -90.0, 90.0, 3),
+                                           ("exp_blend", -87.0, -0.0, 1)])
 def test_elementary_functions_bitwise(orc, fn, lo, hi, step):
     """Device exp_s/log_s/tanh_s/sigmoid_s equal the oracle's on every float of
-    the range (every `step`-th bit pattern)."""
+    the range (every `step`-th bit pattern); the blend's exp_blend equals the
+    oracle's exp_s on every float of [-87, 0] (N1)."""
     import torch
     import paper_2502_14938_b200 as gp
     r = gp.Renderer(0, 64, 64)
@@ -120,7 +122,7 @@ def test_elementary_functions_bitwise(orc, fn, lo, hi, step):
         for s0 in range(a, b + 1, 1 << 26):
             bits = np.arange(s0, min(b + 1, s0 + (1 << 26)), step, dtype=np.int64).astype(np.uint32)
             x = bits.view(np.float32)
-            ref = orc.elem(fn, x)
+            ref = orc.elem("exp" if fn == "exp_blend" else fn, x)
             got = r.elementary(fn, torch.from_numpy(x).cuda()).cpu().numpy()
             same = (got.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(got) & np.isnan(ref))
             nbad += int((~same).sum())
