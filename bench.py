@@ -100,9 +100,9 @@ def _stage_bytes(s, N, K, W, H, fmt_bytes):
         "cull": N * (16 + 1 + 4) + N / 4.0 + 4 * V + 8 * M,
         # miss id, pos, feat, offs, scale in; alpha + 48-byte pool record out per slot
         "derive": M * (4 + 16 + 32 + 120 + 12) + M * K * (4 + 48),
-        # project: ids, alpha per slot, pool per live slot (C/2), 72-byte record per splat;
-        # tiles: 36 B read + 8 B written per splat, 4 B per kept tile
-        "project": 4 * V + 4 * V * K + 48 * (C / 2.0) + 72 * C + 44 * C + 4 * P,
+        # live: ids + alpha per slot in, live id out; project: live id, alpha, 48-byte pool record in,
+        # 72-byte record per splat out; tiles: 36 B read + 8 B written per splat, 4 B per kept tile
+        "project": 4 * V + 4 * V * K + 4 * (C / 2.0) + (4 + 4 + 48) * (C / 2.0) + 72 * C + 44 * C + 4 * P,
         "depth_sort": 12 * C + 3 * 16 * C,
         # pairoff 12 B per splat; expand 12 B per pair + 12 B per splat
         "emit": 24 * C + 12 * P,
@@ -216,7 +216,7 @@ def run_gsc(args):
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
                 "note": f"algorithmic bytes/frame {algo[dom] / nf:.4g}; peak {peaks['src']}"}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    kernels = {"blend": ["blend_kernel"], "project": ["project_kernel", "tiles_kernel"], "cull": ["cull_classify_kernel"],
+    kernels = {"blend": ["blend_kernel"], "project": ["live_kernel", "project_kernel", "tiles_kernel"], "cull": ["cull_classify_kernel"],
                "derive": ["derive_mma_kernel"], "depth_sort": ["onesweep_pass_kernel"] * 4,
                "tile_sort": ["onesweep_pass_kernel"] * 2, "emit": ["pairoff_kernel", "expand_kernel"],
                "ranges": ["ranges_kernel"]}

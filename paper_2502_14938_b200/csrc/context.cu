@@ -27,8 +27,8 @@ int cull_tiles(int N);
 void launch_derive(const float pu[3], const uint32_t *, const float4 *, const int8_t *, const float *, const float *,
                    const int8_t *, const int32_t *, const int8_t *, const int32_t *, float *, float4 *,
                    FrameCounters *, int, bool, cudaStream_t);
-void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, const SplatBufs &, uint32_t *,
-                    FrameCounters *, int, cudaStream_t);
+void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, uint32_t *, const SplatBufs &,
+                    uint32_t *, FrameCounters *, int, cudaStream_t);
 int project_tile_size();
 void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, const uint32_t *,
                      uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
@@ -97,7 +97,7 @@ struct gsc_ctx {
   DevBuf<float4> spA, spB, spC;
   DevBuf<float2> spD;
   DevBuf<uint2> box;
-  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list;
+  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list, live_g;
   DevBuf<uint32_t> pkey_a, pval_a, pkey_b, pval_b;
   DevBuf<uint2> ranges;
   DevBuf<uint32_t> sort_status_a, sort_status_b;
@@ -302,6 +302,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->box.alloc(ctx->cap_splat));
   CU(ctx->count.alloc(ctx->cap_splat));
   CU(ctx->gslot.alloc(ctx->cap_splat));
+  CU(ctx->live_g.alloc(ctx->cap_splat / 2));
   CU(ctx->dkey_a.alloc(ctx->cap_splat));
   CU(ctx->dval_a.alloc(ctx->cap_splat));
   CU(ctx->dkey_b.alloc(ctx->cap_splat));
@@ -427,7 +428,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   // a4
   SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
                ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
-  launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, sb,
+  launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, ctx->live_g.p, sb,
                  reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
   mark();
   // a5 (depth digits of the (tile, depth) sort)

@@ -282,90 +282,9 @@ __device__ __forceinline__ int ilogb_bits(float x) {
   return -127 - (__clz(b) - 9);                           // subnormal: 2^-126 * 0.m
 }
 
-// ---- the exact tile test (O-5 R14), shared by project and emit ----
+// ---- constants of the extent / tile test / blend (R14, N5-N7) ----
 constexpr float kKappa = 1.0009765625f;   // 1 + 2^-10
 constexpr float kSlack = 0.015625f;       // 2^-6
 constexpr float kAlphaMin = 0.0039215688593685626983642578125f;  // fp32(1/255)
-
-// R14: t* = -(Q d) * fl(1/R) (reciprocal rounded once, precomputable per splat)
-__device__ __forceinline__ float edge_q(float d, float lo, float hi, float P, float Q, float R, float invR) {
-  float t = __fmul_rn(-__fmul_rn(Q, d), invR);
-  t = fminf(fmaxf(t, lo), hi);
-  return __fadd_rn(__fadd_rn(__fmul_rn(P, __fmul_rn(d, d)), __fmul_rn(2.0f, __fmul_rn(Q, __fmul_rn(d, t)))),
-                   __fmul_rn(R, __fmul_rn(t, t)));
-}
-
-__device__ __forceinline__ bool tile_kept(float u, float v, float A, float B, float C, float invA, float invC,
-                                          float thr, int tx, int ty, int width, int height) {
-  int px1 = min(16 * tx + 15, width - 1), py1 = min(16 * ty + 15, height - 1);
-  float X0 = __fadd_rn((float)(16 * tx), 0.5f), X1 = __fadd_rn((float)px1, 0.5f);
-  float Y0 = __fadd_rn((float)(16 * ty), 0.5f), Y1 = __fadd_rn((float)py1, 0.5f);
-  if (u >= X0 && u <= X1 && v >= Y0 && v <= Y1) return true;  // q_min = 0 <= thr
-  float dx0 = __fsub_rn(X0, u), dx1 = __fsub_rn(X1, u), dy0 = __fsub_rn(Y0, v), dy1 = __fsub_rn(Y1, v);
-  float q = edge_q(dx0, dy0, dy1, A, B, C, invC);
-  q = fminf(q, edge_q(dx1, dy0, dy1, A, B, C, invC));
-  q = fminf(q, edge_q(dy0, dx0, dx1, C, B, A, invA));
-  q = fminf(q, edge_q(dy1, dx0, dx1, C, B, A, invA));
-  return q <= thr;
-}
-
-// ---- warp-flattened tile enumeration (load balance for the heavy-tailed
-// box sizes: 1.4% of splats carry ~40% of the pairs at ground level).
-// The 32 lanes' candidate boxes are laid end to end (lane order, tiles
-// row-major inside a box) and the warp walks that list 32 items at a time,
-// so a full-screen splat costs its box/32 iterations instead of stalling
-// one lane.  Item order equals the output order of the pairs.
-struct WarpTiles {
-  float u[32], v[32], A[32], B[32], C[32], thr[32], iA[32], iC[32];
-  int tx0[32], ty0[32], bw[32];
-  uint32_t bwm[32];          // magic multiplier: k / bw = umulhi(k, bwm) for k * bw < 2^32
-  uint32_t excl[32], cnt[32], all[32];
-  uint32_t id[32], kb[32];   // emit: splat index and key base (eye * T_e) of the owner
-};
-
-struct TileJob {
-  float u, v, A, B, C, thr;
-  int tx0, ty0, bw, bh;
-};
-
-// stage the lane's job; returns the warp's total number of items
-__device__ __forceinline__ uint32_t warp_tiles_stage(WarpTiles &ws, bool has, const TileJob &j, uint32_t known_cnt) {
-  const uint32_t lane = lane_id();
-  uint32_t nb = has ? (uint32_t)(j.bw * j.bh) : 0u;
-  uint32_t inc = nb;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
-    if (lane >= (uint32_t)o) inc += t;
-  }
-  ws.excl[lane] = inc - nb;
-  ws.u[lane] = j.u; ws.v[lane] = j.v; ws.A[lane] = j.A; ws.B[lane] = j.B; ws.C[lane] = j.C; ws.thr[lane] = j.thr;
-  ws.tx0[lane] = j.tx0; ws.ty0[lane] = j.ty0; ws.bw[lane] = has ? j.bw : 1;
-  ws.bwm[lane] = 0xFFFFFFFFu / (uint32_t)(has ? j.bw : 1) + 1u;
-  ws.iA[lane] = has ? __fdiv_rn(1.0f, j.A) : 0.0f;
-  ws.iC[lane] = has ? __fdiv_rn(1.0f, j.C) : 0.0f;
-  ws.cnt[lane] = 0;
-  ws.all[lane] = has && known_cnt == nb;   // every candidate tile known to be kept: skip the test
-  __syncwarp();
-  return __shfl_sync(0xFFFFFFFFu, inc, 31);
-}
-
-// item w -> owning lane (largest lane with excl <= w), tile, kept?
-__device__ __forceinline__ bool warp_tiles_item(const WarpTiles &ws, uint32_t w, int width, int height, int &owner,
-                                                int &tx, int &ty) {
-  int lo = 0;
-#pragma unroll
-  for (int step = 16; step > 0; step >>= 1)
-    if (ws.excl[lo + step] <= w) lo += step;
-  owner = lo;
-  const uint32_t k = w - ws.excl[lo];
-  const uint32_t bw = (uint32_t)ws.bw[lo];
-  const uint32_t r = bw == 1 ? k : __umulhi(k, ws.bwm[lo]);   // exact: k < 8160 * 68, bw <= 120
-  ty = ws.ty0[lo] + (int)r;
-  tx = ws.tx0[lo] + (int)(k - r * bw);
-  if (ws.all[lo]) return true;
-  return tile_kept(ws.u[lo], ws.v[lo], ws.A[lo], ws.B[lo], ws.C[lo], ws.iA[lo], ws.iC[lo], ws.thr[lo], tx, ty,
-                   width, height);
-}
 
 }  // namespace gsc

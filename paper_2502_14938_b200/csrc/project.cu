@@ -4,22 +4,24 @@
 // tile-coverage count (FlashGS citation), both eyes batched
 // ("independently or in batching"; R19).
 //
-// Warp-centric and barrier-free: each warp acquires its own tile of 64 visible
-// slots s = v*K + j (Gaussian g = X_f[v]*K + j), 2 per lane.  A dead slot
-// costs its 4-byte alpha read; a live one adds its 48-byte pool record.
-// Splats whose candidate tile box is non-empty are compacted in (eye, s)
-// order -- the order that makes the later stable sorts break depth ties by g
-// like the oracle -- with a warp-level decoupled look-back whose aggregate is
-// published BEFORE the expensive kept-tile count, so a warp holding a huge
-// splat never stalls its successors.  Fused: the 4 x 256-bin digit histogram
-// of the depth keys (first pass of the onesweep depth sort) and the pair count.
+// Two kernels.  live_kernel compacts the LIVE visible slots s = v*K + j
+// (255 alpha > 1; Gaussian g = X_f[v]*K + j) into live_g, in s order (hence
+// ascending g), with a CTA-level decoupled look-back over 4096-slot tiles: it
+// only reads 4 bytes per slot, so its look-back chain is short.
+// project_kernel then projects live item i for both eyes with every lane busy
+// and writes splat c = e * n_live + i: per eye, c ascends with g -- the order
+// that makes the later stable sorts break depth ties by g like the oracle.
+// Live splats that project nowhere keep an entry with an empty box (0 tiles).
+// Fused: the 4 x 256-bin digit histogram of the depth keys (first pass of the
+// onesweep depth sort).
 #include "gsc_internal.cuh"
 
 namespace gsc {
 
 constexpr int kPThreads = 256;
-constexpr int kPItems = 1;
-constexpr int kPTile = 32 * kPItems;   // slots per warp tile
+constexpr int kLThreads = 256;
+constexpr int kLRounds = 16;                      // 32-slot rounds per warp
+constexpr int kLTile = kLThreads * kLRounds;      // 4096 slots per CTA tile
 
 struct SplatOut {
   float u, v, A, B, C, thr;
@@ -89,148 +91,106 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   return true;
 }
 
-// Test the 32 lanes' candidate boxes (balanced walk), count the kept tiles per
-// lane and append their keys to the kept-tile list: the warp bump-allocates
-// `total` slots (an upper bound), kept keys are written contiguously in walk
-// order, so lane l's keys start at base + sum of the kept counts of lanes < l.
-__device__ __forceinline__ uint32_t warp_count_list(WarpTiles &ws, bool has, const SplatOut &o, uint32_t kb,
-                                                    int width, int height, int TW, uint32_t *list, uint32_t list_cap,
-                                                    uint32_t *list_top, uint32_t *overflow, uint32_t &list_off) {
-  TileJob j;
-  j.u = o.u; j.v = o.v; j.A = o.A; j.B = o.B; j.C = o.C; j.thr = o.thr;
-  j.tx0 = (int)(o.box_x & 0xFFFFu); j.ty0 = (int)(o.box_y & 0xFFFFu);
-  j.bw = (int)(o.box_x >> 16) - j.tx0 + 1; j.bh = (int)((o.box_y >> 16) & 0x7FFFu) - j.ty0 + 1;
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
-  ws.kb[lane] = kb;   // key base of the lane's eye; items are keyed with their OWNER's base
-  const uint32_t total = warp_tiles_stage(ws, has, j, 0xFFFFFFFFu);
-  uint32_t base = 0;
-  if (lane == 0) {
-    base = atomicAdd(list_top, total);
-    if (base + total > list_cap || base + total < base) atomicExch(overflow, 1u);
-  }
-  base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  uint32_t run = base;
-  for (uint32_t w0 = 0; w0 < total; w0 += 32) {
-    const uint32_t w = w0 + lane;
-    int owner = 0, tx = 0, ty = 0;
-    const bool kept = w < total && warp_tiles_item(ws, w, width, height, owner, tx, ty);
-    const uint32_t mask = __ballot_sync(0xFFFFFFFFu, kept);
-    if (kept) {
-      atomicAdd(&ws.cnt[owner], 1u);
-      const uint32_t pos = run + __popc(mask & lt);
-      if (pos < list_cap) list[pos] = ws.kb[owner] + (uint32_t)(ty * TW + tx);
-    }
-    run += __popc(mask);
-  }
-  __syncwarp();
-  const uint32_t n = has ? ws.cnt[lane] : 0u;
-  __syncwarp();
-  uint32_t inc = n;
+__global__ void __launch_bounds__(kLThreads)
+live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alpha, uint32_t *__restrict__ live_g,
+            uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_cnt[kLThreads / 32], s_pre, s_tile;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
+  const uint32_t S = ctr->n_visible * (uint32_t)kK;
+  const uint32_t ntiles = (S + kLTile - 1) / kLTile;
+  for (;;) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_project, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
+    if (tile >= ntiles) break;
+    uint32_t g[kLRounds], m[kLRounds], cnt = 0;
+    const uint32_t s0 = tile * kLTile + warp * (32 * kLRounds) + lane;
 #pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-    if (lane >= (uint32_t)off) inc += t;
+    for (int r = 0; r < kLRounds; ++r) {
+      const uint32_t s = s0 + 32 * r;
+      float al = 0.0f;
+      g[r] = 0;
+      if (s < S) {
+        const uint32_t v = s / kK, j = s - v * kK;
+        g[r] = visible[v] * kK + j;
+        al = alpha[g[r]];
+      }
+      m[r] = __ballot_sync(0xFFFFFFFFu, __fmul_rn(255.0f, al) > 1.0f);
+      cnt += __popc(m[r]);
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (warp == 0) {
+      const uint32_t c = lane < kLThreads / 32 ? s_cnt[lane] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
+        if (lane >= (uint32_t)off) inc += t;
+      }
+      const uint32_t agg = __shfl_sync(0xFFFFFFFFu, inc, 31);
+      if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
+      uint32_t pre = 0;
+      if (tile > 0) {
+        pre = lookback_u32(status, tile);
+        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+      }
+      if (lane == 0 && tile == ntiles - 1) ctr->n_splat = 2 * (pre + agg);
+      if (lane < kLThreads / 32) s_cnt[lane] = pre + inc - c;   // the warp's exclusive offset
+    }
+    __syncthreads();
+    uint32_t base = s_cnt[warp];
+#pragma unroll
+    for (int r = 0; r < kLRounds; ++r) {
+      if ((m[r] >> lane) & 1u) live_g[base + __popc(m[r] & lt)] = g[r];
+      base += __popc(m[r]);
+    }
+    __syncthreads();   // s_cnt / s_tile reuse
   }
-  list_off = base + inc - n;
-  return n;
 }
 
 __global__ void __launch_bounds__(kPThreads)
-project_kernel(FrameC fc, const uint32_t *__restrict__ visible, const float *__restrict__ alpha,
-               const float4 *__restrict__ pool, SplatBufs sb, uint32_t *__restrict__ status,
-               FrameCounters *__restrict__ ctr) {
+project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__restrict__ alpha,
+               const float4 *__restrict__ pool, SplatBufs sb, FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_hist[4][256];
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
   __syncthreads();
-  const uint32_t S = ctr->n_visible * (uint32_t)kK;
-  const uint32_t ntiles = (S + kPTile - 1) / kPTile;
-
-  for (;;) {
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&ctr->tile_project, 1u);
-    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
-    if (tile >= ntiles) break;
-
-    SplatOut so[kPItems][2];
-    bool ok[kPItems][2], live[kPItems];
-    uint32_t gs[kPItems];
-    float4 q2[kPItems];
-    float al[kPItems];
-    // compaction is over LIVE slots (255 alpha > 1), both eyes: the tile's
-    // aggregate is known after the 4-byte alpha reads and is published before
-    // the projection math, so the look-back never waits on a predecessor's
-    // arithmetic.  Live splats that project nowhere keep an entry with 0 tiles.
-    uint32_t m[kPItems], agg = 0;
+  const uint32_t n_live = ctr->n_splat / 2;
+  for (uint32_t i = blockIdx.x * kPThreads + threadIdx.x; i < n_live; i += gridDim.x * kPThreads) {
+    const uint32_t g = live_g[i];
+    const float al = alpha[g];
+    const float4 q0 = pool[3 * (size_t)g];
+    const float4 q1 = pool[3 * (size_t)g + 1];
+    const float4 q2 = pool[3 * (size_t)g + 2];
 #pragma unroll
-    for (int it = 0; it < kPItems; ++it) {
-      const uint32_t s = tile * kPTile + it * 32 + lane;
-      al[it] = 0.0f;
-      gs[it] = 0;
-      if (s < S) {
-        uint32_t v = s / kK, j = s - v * kK;
-        uint32_t g = visible[v] * kK + j;
-        gs[it] = g;
-        al[it] = alpha[g];
+    for (int e = 0; e < 2; ++e) {
+      SplatOut o;
+      const bool ok = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, o);
+      const uint32_t c = (uint32_t)e * n_live + i;
+      uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
+      if (ok) {
+        // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
+        // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
+        const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+        dk = __float_as_uint(o.depth);
+        sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
+        sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
+        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
+        // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
+        // outside them has power < pmin, so the blend may skip it without changing a decision
+        const float qmax = __fmul_rn(-2.0f, pmin);
+        const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
+        const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
+        sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
+        sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
+      } else {
+        sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
       }
-      live[it] = __fmul_rn(255.0f, al[it]) > 1.0f;
-      m[it] = __ballot_sync(0xFFFFFFFFu, live[it]);
-      agg += 2 * __popc(m[it]);
+      sb.depth[c] = dk;
+      sb.gslot[c] = g;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
     }
-    if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-#pragma unroll
-    for (int it = 0; it < kPItems; ++it) {
-      ok[it][0] = ok[it][1] = false;
-      if (live[it]) {
-        const size_t g = gs[it];
-        const float4 q0 = pool[3 * g];
-        const float4 q1 = pool[3 * g + 1];
-        q2[it] = pool[3 * g + 2];
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-          ok[it][e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al[it], q0, q1, q2[it], so[it][e]);
-      }
-    }
-    uint32_t pre = 0;
-    if (tile > 0) {
-      pre = lookback_u32(status, tile);
-      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-    }
-    if (lane == 0 && tile == ntiles - 1) ctr->n_splat = pre + agg;
-    uint32_t base = pre;
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-#pragma unroll
-      for (int it = 0; it < kPItems; ++it) {
-        if (live[it]) {
-          const SplatOut &o = so[it][e];
-          const uint32_t c = base + __popc(m[it] & lt);
-          uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
-          if (ok[it][e]) {
-            // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, thr, depth)
-            // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
-            const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
-            dk = __float_as_uint(o.depth);
-            sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
-            sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al[it], q2[it].y);
-            sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-            // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
-            // outside them has power < pmin, so the blend may skip it without changing a decision
-            const float qmax = __fmul_rn(-2.0f, pmin);
-            const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
-            const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
-            sb.spC[c] = make_float4(q2[it].z, q2[it].w, rx, ry);
-            sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
-          } else {
-            sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
-          }
-          sb.depth[c] = dk;
-          sb.gslot[c] = gs[it];
-#pragma unroll
-          for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
-        }
-        base += __popc(m[it]);
-      }
   }
   // flush the fused histogram
   __syncthreads();
@@ -400,20 +360,24 @@ tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
   if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
 }
 
-static int g_project_grid = 0, g_tiles_grid = 0;
+static int g_live_grid = 0, g_project_grid = 0, g_tiles_grid = 0;
 
 void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
-                    const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms, cudaStream_t st) {
+                    uint32_t *live_g, const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms,
+                    cudaStream_t st) {
   if (g_project_grid == 0) {
     int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, live_kernel, kLThreads, 0);
+    g_live_grid = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel, kPThreads, 0);
     g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_kernel, kPThreads, 0);
     g_tiles_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
-  project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, visible, alpha, pool, sb, status, ctr);
+  live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_g, status, ctr);
+  project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr);
   tiles_kernel<<<g_tiles_grid, kPThreads, 0, st>>>(fc, sb, ctr);
 }
-int project_tile_size() { return kPTile; }
+int project_tile_size() { return kLTile; }
 
 }  // namespace gsc
