@@ -12,7 +12,7 @@
 //
 // Onesweep pass (Adinets & Merrill 2022 style): one kernel per 8-bit digit;
 // tiles of 4096 keys acquired in launch order through an atomic counter;
-// stable block-local ranking by warp match_any; per-digit decoupled look-back
+// stable block-local ranking (per-warp digit peer masks by shared atomicOr); per-digit decoupled look-back
 // across tiles; scatter through shared memory for coalesced writes.  The
 // global digit histograms come fused from the producing kernel (project for
 // depth keys, emit for tile keys).  Look-back status words live in two
@@ -33,6 +33,7 @@ struct SortSmem {
   uint32_t keys[kSTile];
   uint32_t vals[kSTile];
   uint32_t whist[kSWarps][kBins + 4];   // per-warp counts -> exclusive prefixes (bin 256 = invalid)
+  uint32_t match[kSWarps][kBins + 4];   // per-warp lane masks of the current item's digit (kept zero)
   uint32_t blk_off[kBins];
   uint32_t gbase[kBins];
   uint32_t tile;
@@ -69,6 +70,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
     s_hex[t] = wp + inc - h;
   }
 
+  for (int k = t; k < kSWarps * (kBins + 4); k += kSThreads) (&S.match[0][0])[k] = 0;
   for (;;) {
     __syncthreads();
     if (t == 0) S.tile = atomicAdd(tile_ctr, 1u);
@@ -88,11 +90,18 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
     for (int i = 0; i < kSItems; ++i) {
       uint32_t idx = wbase + i * 32 + lane;
       uint32_t d = idx < n ? (key[i] >> shift) & 0xFFu : (uint32_t)kBins;
-      uint32_t peers = __match_any_sync(0xFFFFFFFFu, d);
-      uint32_t before = S.whist[warp][d];
+      // peers = lanes holding the same digit: OR the lane bits into a per-digit shared word
+      // (faster than match.any.sync here), then the lowest peer updates the count and clears it
+      atomicOr(&S.match[warp][d], 1u << lane);
+      __syncwarp();
+      const uint32_t peers = S.match[warp][d];
+      const uint32_t before = S.whist[warp][d];
       rank[i] = before + __popc(peers & lt);
       __syncwarp();
-      if (lane == (uint32_t)(__ffs(peers) - 1)) S.whist[warp][d] = before + __popc(peers);
+      if ((peers & lt) == 0) {
+        S.whist[warp][d] = before + __popc(peers);
+        S.match[warp][d] = 0;
+      }
       __syncwarp();
     }
     __syncthreads();
