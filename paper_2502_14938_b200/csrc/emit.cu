@@ -7,7 +7,7 @@
 // order ("key-value pairs").
 //
 //   pairoff: exclusive scan of the kept-tile counts in depth order
-//            (warp-level decoupled look-back) -> pair_off[p], P
+//            (CTA tiles of 4096, CTA-wide decoupled look-back) -> pair_off[p], P
 //   expand : load-balanced expansion -- each warp owns 256 consecutive OUTPUT
 //            positions q and finds the owning splat by a 32-ary cooperative
 //            search of pair_off, so the heavy-tailed splat sizes (near splats
@@ -20,25 +20,28 @@
 namespace gsc {
 
 constexpr int kXThreads = 256;
-constexpr int kOffItems = 8;
-constexpr int kOffTile = 32 * kOffItems;   // sorted positions per warp tile
+constexpr int kOffItems = 16;
+constexpr int kOffTile = kXThreads * kOffItems;   // 4096 sorted positions per CTA tile
 constexpr int kExpItems = 8;
 constexpr int kExpChunk = 32 * kExpItems;  // output positions per warp chunk
 
 __global__ void __launch_bounds__(kXThreads)
 pairoff_kernel(EmitIn in, uint32_t cap, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
+  __shared__ uint32_t s_cnt[kXThreads / 32], s_red[kXThreads / 32 + 1], s_tile;
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t C = ctr->n_splat;
   const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
   for (;;) {
-    uint32_t tile = 0;
-    if (lane == 0) tile = atomicAdd(&ctr->tile_pairoff, 1u);
-    tile = __shfl_sync(0xFFFFFFFFu, tile, 0);
+    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_pairoff, 1u);
+    __syncthreads();
+    const uint32_t tile = s_tile;
     if (tile >= ntiles) break;
+    // warp w owns positions [tile*4096 + w*512, +512), 16 rounds of 32
+    const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;
     uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
 #pragma unroll
     for (int i = 0; i < kOffItems; ++i) {
-      const uint32_t p = tile * kOffTile + i * 32 + lane;
+      const uint32_t p = p0 + 32 * i;
       cnt[i] = p < C ? in.count[in.sorted[p]] : 0u;
     }
 #pragma unroll
@@ -46,32 +49,38 @@ pairoff_kernel(EmitIn in, uint32_t cap, uint32_t *__restrict__ status, FrameCoun
       uint32_t inc = cnt[i];
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
-        uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
         if (lane >= (uint32_t)o) inc += t;
       }
       excl[i] = run + inc - cnt[i];
       run += __shfl_sync(0xFFFFFFFFu, inc, 31);
     }
-    const uint32_t agg = run;
+    if (lane == 0) s_cnt[warp] = run;
+    __syncthreads();
+    uint32_t wex = 0, agg = 0;
+#pragma unroll
+    for (int w = 0; w < kXThreads / 32; ++w) {
+      const uint32_t c = s_cnt[w];
+      wex += (uint32_t)w < warp ? c : 0u;
+      agg += c;
+    }
+    if (threadIdx.x == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
     uint32_t pre = 0;
-    if (tile == 0) {
-      if (lane == 0) st_volatile_u32(status, (2u << 30) | agg);
-    } else {
-      if (lane == 0) st_volatile_u32(status + tile, (1u << 30) | agg);
-      pre = lookback_u32(status, tile);
-      if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+    if (tile > 0) {
+      pre = block_lookback_u32<kXThreads>(status, tile, s_red);
+      if (threadIdx.x == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
     }
 #pragma unroll
     for (int i = 0; i < kOffItems; ++i) {
-      const uint32_t p = tile * kOffTile + i * 32 + lane;
-      if (p < C) in.pair_off[p] = pre + excl[i];
+      const uint32_t p = p0 + 32 * i;
+      if (p < C) in.pair_off[p] = pre + wex + excl[i];
     }
-    if (lane == 0 && tile == ntiles - 1) {
+    if (threadIdx.x == 0 && tile == ntiles - 1) {
       const uint32_t tot = pre + agg;
       ctr->n_pairs = tot < cap ? tot : cap;
       if (tot > cap) ctr->overflow = 1u;
     }
-    (void)lt;
+    __syncthreads();   // s_cnt / s_tile reuse
   }
 }
 

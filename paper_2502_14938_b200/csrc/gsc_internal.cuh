@@ -142,6 +142,47 @@ __device__ __forceinline__ uint32_t lookback_u32(uint32_t *status, uint32_t tile
   return prefix;
 }
 
+// The same look-back run by a whole CTA of kThreads: every thread reads one
+// predecessor status word, so one round trip covers kThreads tiles -- with a
+// persistent grid of ~600 tiles in flight the inclusive frontier lags by
+// about that many tiles, which a 32-wide warp window walks in ~20 serial
+// round trips.  All threads must call it; returns the exclusive prefix in all
+// of them.  `red` is kThreads/32 + 1 words of shared scratch.
+template <int kThreads>
+__device__ __forceinline__ uint32_t block_lookback_u32(uint32_t *status, uint32_t tile, uint32_t *red) {
+  constexpr uint32_t kMask = 0x3FFFFFFFu;
+  constexpr int kW = kThreads / 32;
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  uint32_t prefix = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (base >= 0) {
+    const int64_t idx = base - (int64_t)t;
+    uint32_t s = 2u << 30;   // out of range counts as an inclusive zero
+    if (idx >= 0) {
+      do { s = ld_volatile_u32(status + idx); } while ((s >> 30) == 0);
+    }
+    // nearest inclusive predecessor = smallest thread index holding one
+    const uint32_t incl = __ballot_sync(0xFFFFFFFFu, (s >> 30) == 2u);
+    if (lane == 0) red[warp] = incl ? warp * 32 + (uint32_t)(__ffs(incl) - 1) : (uint32_t)kThreads;
+    __syncthreads();
+    uint32_t upto = kThreads;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) upto = min(upto, red[w]);
+    uint32_t v = t <= upto ? (s & kMask) : 0u;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kW; ++w) prefix += red[w];
+    __syncthreads();
+    if (upto < (uint32_t)kThreads) break;
+    base -= kThreads;
+  }
+  return prefix;
+}
+
 // 64-bit status: [63:62] flag, [61:31] field b, [30:0] field a (two counts).
 __device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *status, uint32_t tile) {
   constexpr unsigned long long kMask = (1ull << 62) - 1;

@@ -94,7 +94,7 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
 __global__ void __launch_bounds__(kLThreads)
 live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alpha, uint32_t *__restrict__ live_g,
             uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_cnt[kLThreads / 32], s_pre, s_tile;
+  __shared__ uint32_t s_cnt[kLThreads / 32], s_red[kLThreads / 32 + 1], s_tile;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
   const uint32_t S = ctr->n_visible * (uint32_t)kK;
   const uint32_t ntiles = (S + kLTile - 1) / kLTile;
@@ -120,26 +120,21 @@ live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alph
     }
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
-    if (warp == 0) {
-      const uint32_t c = lane < kLThreads / 32 ? s_cnt[lane] : 0u;
-      uint32_t inc = c;
+    uint32_t wex = 0, agg = 0;
 #pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-        if (lane >= (uint32_t)off) inc += t;
-      }
-      const uint32_t agg = __shfl_sync(0xFFFFFFFFu, inc, 31);
-      if (lane == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-      uint32_t pre = 0;
-      if (tile > 0) {
-        pre = lookback_u32(status, tile);
-        if (lane == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-      }
-      if (lane == 0 && tile == ntiles - 1) ctr->n_splat = 2 * (pre + agg);
-      if (lane < kLThreads / 32) s_cnt[lane] = pre + inc - c;   // the warp's exclusive offset
+    for (int w = 0; w < kLThreads / 32; ++w) {
+      const uint32_t c = s_cnt[w];
+      wex += (uint32_t)w < warp ? c : 0u;
+      agg += c;
     }
-    __syncthreads();
-    uint32_t base = s_cnt[warp];
+    if (threadIdx.x == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
+    uint32_t pre = 0;
+    if (tile > 0) {
+      pre = block_lookback_u32<kLThreads>(status, tile, s_red);
+      if (threadIdx.x == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
+    }
+    if (threadIdx.x == 0 && tile == ntiles - 1) ctr->n_splat = 2 * (pre + agg);
+    uint32_t base = pre + wex;
 #pragma unroll
     for (int r = 0; r < kLRounds; ++r) {
       if ((m[r] >> lane) & 1u) live_g[base + __popc(m[r] & lt)] = g[r];
