@@ -443,12 +443,13 @@ int orc_row_interval(const orc_config *cfg, const orc_splat *s, int ty, float *x
   if (!(lo <= hi)) return 0;
   float bs = s->B * sd;
   float at = s->A * s->thr;
+  float invA = 1.0f / s->A;                          /* rounded once per splat (N7) */
   float dyr = fminf(fmaxf(-bs, lo), hi);
   float Dr = fmaxf(at - (det * (dyr * dyr)), 0.0f);
-  *xr = s->u + ((sqrtf(Dr) - (s->B * dyr)) / s->A);
+  *xr = s->u + ((sqrtf(Dr) - (s->B * dyr)) * invA);
   float dyl = fminf(fmaxf(bs, lo), hi);
   float Dl = fmaxf(at - (det * (dyl * dyl)), 0.0f);
-  *xl = s->u - ((sqrtf(Dl) + (s->B * dyl)) / s->A);
+  *xl = s->u - ((sqrtf(Dl) + (s->B * dyl)) * invA);
   return 1;
 }
 

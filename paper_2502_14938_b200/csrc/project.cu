@@ -144,93 +144,46 @@ live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alph
   }
 }
 
-__global__ void __launch_bounds__(kPThreads)
-project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__restrict__ alpha,
-               const float4 *__restrict__ pool, SplatBufs sb, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_hist[4][256];
-  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
-  __syncthreads();
-  const uint32_t n_live = ctr->n_splat / 2;
-  for (uint32_t i = blockIdx.x * kPThreads + threadIdx.x; i < n_live; i += gridDim.x * kPThreads) {
-    const uint32_t g = live_g[i];
-    const float al = alpha[g];
-    const float4 q0 = pool[3 * (size_t)g];
-    const float4 q1 = pool[3 * (size_t)g + 1];
-    const float4 q2 = pool[3 * (size_t)g + 2];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      SplatOut o;
-      const bool ok = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, o);
-      const uint32_t c = (uint32_t)e * n_live + i;
-      uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
-      if (ok) {
-        // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
-        // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
-        const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
-        dk = __float_as_uint(o.depth);
-        sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
-        sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
-        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-        // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
-        // outside them has power < pmin, so the blend may skip it without changing a decision
-        const float qmax = __fmul_rn(-2.0f, pmin);
-        const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
-        const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
-        sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
-        sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
-      } else {
-        sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
-      }
-      sb.depth[c] = dk;
-      sb.gslot[c] = g;
-#pragma unroll
-      for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
-    }
-  }
-  // flush the fused histogram
-  __syncthreads();
-  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) {
-    uint32_t v = (&s_hist[0][0])[k];
-    if (v) atomicAdd(&ctr->hist_depth[0][0] + k, v);
-  }
-}
-
 // ---- row form of the exact tile test (R14 / N7), one row of one splat per item
 struct WarpRows {
-  float u[32], v[32], A[32], B[32], thr[32], det[32], ey[32], bs[32];
+  float u[32], v[32], B[32], det[32], ey[32], bs[32], at[32], invA[32], xr_ext[32], xl_ext[32];
   int tx0[32], tx1[32], ty0[32];
   uint32_t excl[32], cnt[32], kb[32];
 };
 
-// x-interval [xl, xr] of the ellipse {q <= thr} over the pixel-centre rows of tile row ty
+// x-interval [xl, xr] of the ellipse {q <= thr} over the pixel-centre rows of tile row ty.  When the
+// band contains the extreme rows dy = -/+ B s (the usual case) the clamps are inactive and the per-row
+// expression equals the per-splat xr_ext / xl_ext bit for bit.
 __device__ __forceinline__ bool row_interval(const WarpRows &ws, int o, int ty, int height, float &xl, float &xr) {
-  const float A = ws.A[o], B = ws.B[o], det = ws.det[o], ey = ws.ey[o], bs = ws.bs[o], v = ws.v[o], u = ws.u[o];
+  const float ey = ws.ey[o], bs = ws.bs[o], v = ws.v[o];
   const int py1 = min(16 * ty + 15, height - 1);
   const float Y0 = __fadd_rn((float)(16 * ty), 0.5f), Y1 = __fadd_rn((float)py1, 0.5f);
   const float lo = fmaxf(__fsub_rn(Y0, v), -ey), hi = fminf(__fsub_rn(Y1, v), ey);
   if (!(lo <= hi)) return false;
-  const float at = __fmul_rn(A, ws.thr[o]);
-  const float dyr = fminf(fmaxf(-bs, lo), hi);
-  const float Dr = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyr, dyr))), 0.0f);
-  xr = __fadd_rn(u, __fdiv_rn(__fsub_rn(__fsqrt_rn(Dr), __fmul_rn(B, dyr)), A));
-  const float dyl = fminf(fmaxf(bs, lo), hi);
-  const float Dl = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyl, dyl))), 0.0f);
-  xl = __fsub_rn(u, __fdiv_rn(__fadd_rn(__fsqrt_rn(Dl), __fmul_rn(B, dyl)), A));
+  const float dyr = fminf(fmaxf(-bs, lo), hi), dyl = fminf(fmaxf(bs, lo), hi);
+  xr = ws.xr_ext[o];
+  xl = ws.xl_ext[o];
+  if (dyr != -bs || dyl != bs) {
+    const float u = ws.u[o], B = ws.B[o], det = ws.det[o], at = ws.at[o], invA = ws.invA[o];
+    const float Dr = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyr, dyr))), 0.0f);
+    xr = __fadd_rn(u, __fmul_rn(__fsub_rn(__fsqrt_rn(Dr), __fmul_rn(B, dyr)), invA));
+    const float Dl = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyl, dyl))), 0.0f);
+    xl = __fsub_rn(u, __fmul_rn(__fadd_rn(__fsqrt_rn(Dl), __fmul_rn(B, dyl)), invA));
+  }
   return true;
 }
 
-// kept columns of row ty inside the candidate box [tx0, tx1]: X0(tx) <= xr and X1(tx) >= xl
+// kept columns [a, b] of row ty inside the candidate box [tx0, tx1]: X0(tx) <= xr and X1(tx) >= xl with
+// X0 = 16 tx + 0.5, X1 = min(16 tx + 15, W - 1) + 0.5.  b = floor((xr - 0.5)/16) and
+// a = ceil((xl - 15.5)/16) are exact: for xr >= 0.5 (xl >= 7.75) the subtraction is exact (Sterbenz /
+// ulp <= 0.5) and the scaling by 2^-4 too; below that the predicate holds for no (every) column >= 0
+// whatever the rounding.  Only the image's last column has a smaller X1: checked explicitly.
 __device__ __forceinline__ void row_cols(float xl, float xr, int tx0, int tx1, int width, int &a, int &b) {
-  auto X0 = [](int tx) { return __fadd_rn((float)(16 * tx), 0.5f); };
-  auto X1 = [width](int tx) { return __fadd_rn((float)min(16 * tx + 15, width - 1), 0.5f); };
-  float fa = ceilf(__fmul_rn(__fsub_rn(xl, 15.5f), 0.0625f));
-  float fb = floorf(__fmul_rn(__fsub_rn(xr, 0.5f), 0.0625f));
-  a = (int)fminf(fmaxf(fa, (float)tx0), (float)tx1 + 1.0f);
+  const float fb = floorf(__fmul_rn(__fsub_rn(xr, 0.5f), 0.0625f));
+  const float fa = ceilf(__fmul_rn(__fsub_rn(xl, 15.5f), 0.0625f));
   b = (int)fminf(fmaxf(fb, (float)tx0 - 1.0f), (float)tx1);
-  while (a > tx0 && X1(a - 1) >= xl) --a;         // exact predicate decides at the edges
-  while (a <= tx1 && X1(a) < xl) ++a;
-  while (b < tx1 && X0(b + 1) <= xr) ++b;
-  while (b >= tx0 && X0(b) > xr) --b;
+  a = (int)fminf(fmaxf(fa, (float)tx0), (float)tx1 + 1.0f);
+  if (a <= b && __fadd_rn((float)min(16 * a + 15, width - 1), 0.5f) < xl) ++a;
 }
 
 // Rows of the 32 lanes' candidate boxes walked as one list; each row's kept
@@ -258,10 +211,17 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
   ws.kb[lane] = kb;
   if (has) {
     const float det = __fsub_rn(__fmul_rn(o.A, o.C), __fmul_rn(o.B, o.B));
-    ws.u[lane] = o.u; ws.v[lane] = o.v; ws.A[lane] = o.A; ws.B[lane] = o.B; ws.thr[lane] = o.thr;
-    ws.det[lane] = det;
+    const float bs = __fmul_rn(o.B, __fsqrt_rn(__fdiv_rn(o.thr, __fmul_rn(det, o.C))));
+    const float at = __fmul_rn(o.A, o.thr), invA = __fdiv_rn(1.0f, o.A);
+    ws.u[lane] = o.u; ws.v[lane] = o.v; ws.B[lane] = o.B; ws.det[lane] = det; ws.at[lane] = at;
+    ws.invA[lane] = invA;
     ws.ey[lane] = __fsqrt_rn(__fmul_rn(o.thr, __fdiv_rn(o.A, det)));
-    ws.bs[lane] = __fmul_rn(o.B, __fsqrt_rn(__fdiv_rn(o.thr, __fmul_rn(det, o.C))));
+    ws.bs[lane] = bs;
+    // the rows' x-extremes when no clamp is active (dyr = -bs, dyl = bs), same expression as row_interval
+    const float D = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(bs, bs))), 0.0f);
+    const float sD = __fsqrt_rn(D), Bb = __fmul_rn(o.B, bs);
+    ws.xr_ext[lane] = __fadd_rn(o.u, __fmul_rn(__fsub_rn(sD, __fmul_rn(o.B, -bs)), invA));
+    ws.xl_ext[lane] = __fsub_rn(o.u, __fmul_rn(__fadd_rn(sD, Bb), invA));
   }
   ws.tx0[lane] = tx0; ws.tx1[lane] = tx1; ws.ty0[lane] = ty0;
   __syncwarp();
@@ -316,46 +276,88 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
   return n;
 }
 
-// Kept tiles of every compacted splat (rows of the 32 lanes' boxes walked as
-// one list) -> kept count and the kept-tile list (row-major keys
-// eye*T_e + ty*TW + tx).  No ordering constraint between warps: each warp
+// Live item i (32 consecutive per warp) -> both eyes' splat records, then the
+// exact kept-tile walk of the warp's 32 splats per eye (rows of the candidate
+// boxes walked as one list) -> kept count and the kept-tile list (row-major
+// keys eye*T_e + ty*TW + tx).  No ordering constraint between warps: each warp
 // bump-allocates its list space.
 __global__ void __launch_bounds__(kPThreads)
-tiles_kernel(FrameC fc, SplatBufs sb, FrameCounters *__restrict__ ctr) {
-  __shared__ WarpRows s_wt[kPThreads / 32];
+project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__restrict__ alpha,
+               const float4 *__restrict__ pool, SplatBufs sb, FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_hist[4][256];
+  __shared__ WarpRows s_wr[kPThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  WarpRows &ws = s_wt[warp];
-  const uint32_t C = ctr->n_splat;
+  WarpRows &ws = s_wr[warp];
+  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t n_live = ctr->n_splat / 2;
   const uint32_t nw = (gridDim.x * kPThreads) >> 5;
   uint32_t pairs_local = 0;
-  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 32 + warp * 32; base < C; base += nw * 32) {
-    const uint32_t c = base + lane;
-    const bool in = c < C;
-    const uint2 bx = in ? sb.box[c] : make_uint2(0x0000FFFFu, 0u);
-    const bool has = (bx.x >> 16) >= (bx.x & 0xFFFFu);     // dead entries carry an empty box
-    SplatOut o{};
-    uint32_t kb = 0;
-    if (has) {
-      const float4 a = sb.spA[c];
-      o.u = a.x; o.v = a.y; o.A = __fmul_rn(-2.0f, a.z); o.B = -a.w;
-      o.C = __fmul_rn(-2.0f, sb.spB[c].x); o.thr = sb.spD[c].x;
-      o.box_x = bx.x; o.box_y = bx.y & 0x7FFFFFFFu;
-      kb = (bx.y >> 31) ? (uint32_t)fc.Te : 0u;
+  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 32 + warp * 32; base < n_live; base += nw * 32) {
+    const uint32_t i = base + lane;
+    const bool valid = i < n_live;
+    SplatOut so[2];
+    bool ok[2] = {false, false};
+    uint32_t g = 0;
+    float al = 0.0f;
+    float4 q2 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (valid) {
+      g = live_g[i];
+      al = alpha[g];
+      const float4 q0 = pool[3 * (size_t)g];
+      const float4 q1 = pool[3 * (size_t)g + 1];
+      q2 = pool[3 * (size_t)g + 2];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        ok[e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, so[e]);
     }
-    uint32_t loff = 0;
-    const uint32_t n = warp_rows_list(ws, has, o, kb, fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
-                                      &ctr->list_top, &ctr->overflow, loff);
-    if (in) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const SplatOut &o = so[e];
+      uint32_t loff = 0;
+      const uint32_t n = warp_rows_list(ws, ok[e], o, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height, fc.TW,
+                                        sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
+      if (!valid) continue;
+      const uint32_t c = (uint32_t)e * n_live + i;
+      uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
+      if (ok[e]) {
+        // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
+        // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
+        const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+        dk = __float_as_uint(o.depth);
+        sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
+        sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
+        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
+        // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
+        // outside them has power < pmin, so the blend may skip it without changing a decision
+        const float qmax = __fmul_rn(-2.0f, pmin);
+        const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
+        const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
+        sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
+        sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
+      } else {
+        sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
+      }
+      sb.depth[c] = dk;
+      sb.gslot[c] = g;
       sb.count[c] = n;
       sb.list_off[c] = loff;
       pairs_local += n;
+#pragma unroll
+      for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
     }
   }
   for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
   if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
+  // flush the fused histogram
+  __syncthreads();
+  for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) {
+    uint32_t v = (&s_hist[0][0])[k];
+    if (v) atomicAdd(&ctr->hist_depth[0][0] + k, v);
+  }
 }
 
-static int g_live_grid = 0, g_project_grid = 0, g_tiles_grid = 0;
+static int g_live_grid = 0, g_project_grid = 0;
 
 void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
                     uint32_t *live_g, const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms,
@@ -366,12 +368,9 @@ void launch_project(const FrameC &fc, const uint32_t *visible, const float *alph
     g_live_grid = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel, kPThreads, 0);
     g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tiles_kernel, kPThreads, 0);
-    g_tiles_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
   live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_g, status, ctr);
   project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr);
-  tiles_kernel<<<g_tiles_grid, kPThreads, 0, st>>>(fc, sb, ctr);
 }
 int project_tile_size() { return kLTile; }
 
