@@ -4,10 +4,11 @@
 // One 256-thread CTA per (eye, 16x16 tile); warp w owns the 8x4 pixel block
 // at columns 8 (w & 1) .., rows 4 (w >> 1) .., one pixel per lane, and runs
 // independently of the other warps (no block barrier): it walks the tile's
-// depth-sorted pair list in chunks of 32, each lane fetching one splat record
-// (the 8 warps of a CTA hit the same records, so 7 of 8 fetches are L1 hits),
-// keeps the splats whose padded bounding box of {power >= skip bound} touches
-// the block (ballot), stages those records in the warp's SMEM slots,
+// depth-sorted pair list in chunks of 32, keeps the splats whose padded
+// bounding box of {power >= skip bound} touches the block (one bit per block
+// in the pair key, computed by project.cu's tile walk), stages those records
+// in the warp's SMEM slots (the 8 warps of a CTA fetch overlapping records, so
+// most fetches are L1 hits),
 // evaluates them in depth order and leaves as soon as all 32 of its pixels
 // have terminated.  Skipping a (pixel, splat) by the box never changes a
 // decision: outside it power < -ln(255 alpha) - 2^-7, so alpha' < 1/255
@@ -41,7 +42,8 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
 
 template <bool kCount>   // kCount: accumulate n_evals / n_exp (GSC_F_COUNT_EVALS)
 __global__ void __launch_bounds__(kBThreads)
-blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_vals,
+blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
+             const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
   // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
@@ -59,9 +61,6 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const int px = bx0 + (int)(lane & 7), py = by0 + (int)(lane >> 3);
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
-  // this warp's block: pixel centres x in [X0, X1], y in [Y0, Y1]
-  const float X0 = __fadd_rn((float)bx0, 0.5f), X1 = __fadd_rn(X0, 7.0f);
-  const float Y0 = __fadd_rn((float)by0, 0.5f), Y1 = __fadd_rn(Y0, 3.0f);
   const uint2 rg = ranges[tile];
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   // a lane's liveness floor on power: -inf while it composites, +inf once it has terminated (or lies
@@ -76,23 +75,17 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xFFFFFFFFu, pfloor > 0.0f)) break;
     const uint32_t idx = b + lane;
-    bool in = false;
-    uint32_t c = 0;
-    float4 a = make_float4(0.f, 0.f, 0.f, 0.f), cc = a;
-    if (idx < rg.y) {
-      c = pair_vals[idx];
-      a = spA[c];
-      cc = spC[c];
-      in = __fadd_rn(a.x, cc.z) >= X0 && __fsub_rn(a.x, cc.z) <= X1 && __fadd_rn(a.y, cc.w) >= Y0 &&
-           __fsub_rn(a.y, cc.w) <= Y1;
-    }
-    // compact the strip's splats into the warp's slots, depth order preserved
+    // the pair key's block mask (bit = warp) says whether the splat's box of {power >= skip bound}
+    // meets this warp's 8x4 block (computed by project.cu with the fp32 test of DESIGN.md N5)
+    const bool in = idx < rg.y && ((pair_keys[idx] >> (24 + warp)) & 1u);
+    // compact the block's splats into the warp's slots, depth order preserved
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
     if (in) {
+      const uint32_t c = pair_vals[idx];
       const uint32_t slot = __popc(bits & lt);
-      slots[warp][slot] = a;
+      slots[warp][slot] = spA[c];
       slots[warp][32 + slot] = spB[c];
-      slots[warp][64 + slot] = cc;
+      slots[warp][64 + slot] = spC[c];
     }
     const uint32_t n = __popc(bits);
     __syncwarp();
@@ -159,13 +152,14 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   }
 }
 
-void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_vals, const float4 *spA,
+void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_keys, const uint32_t *pair_vals,
+                  const float4 *spA,
                   const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, FrameCounters *ctr,
                   bool count, cudaStream_t st) {
   if (count)
-    blend_kernel<true><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<true><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
   else
-    blend_kernel<false><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<false><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
 }
 
 // elementary-function self test (parity sweeps through the C ABI)

@@ -34,7 +34,8 @@ void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const
                      uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, cudaStream_t);
 void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
-void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const float4 *, const float4 *, const float4 *,
+void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
+                  const float4 *,
                   void *, void *, int, FrameCounters *, bool, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 int sort_tile_size();
@@ -449,7 +450,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   launch_ranges(ctx->pkey_a.p, ctr, ctx->ranges.p, ctx->num_sms, st);
   mark();
   // a8
-  launch_blend(fc, ctx->ranges.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr,
+  launch_blend(fc, ctx->ranges.p, ctx->pkey_a.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr,
                (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, st);
   launch_record(ctr, ctx->rec_dev.p + slot_i, st);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
@@ -649,7 +650,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       for (size_t k = 0; k < np; ++k) {
         uint32_t db;
         std::memcpy(&db, &D[pv[k]].y, 4);
-        out[k] = ((uint64_t)pk[k] << 32) | db;
+        out[k] = ((uint64_t)(pk[k] & 0x00FFFFFFu) << 32) | db;   // bits 24..31: blend block mask
       }
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
       return GSC_OK;

@@ -151,18 +151,20 @@ __global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCoun
   for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < nvec; v0 += stride) {
     const uint32_t v = v0 + threadIdx.x;
     const uint32_t p = 4 * v;
+    // the tile key is the low 24 bits (bits 24..31 carry blend.cu's block mask)
+    constexpr uint32_t kM = 0x00FFFFFFu;
     uint32_t k[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
     if (p + 3 < P) {
       const uint4 q = reinterpret_cast<const uint4 *>(keys)[v];
-      k[0] = q.x; k[1] = q.y; k[2] = q.z; k[3] = q.w;
+      k[0] = q.x & kM; k[1] = q.y & kM; k[2] = q.z & kM; k[3] = q.w & kM;
     } else {
       for (int i = 0; i < 4; ++i)
-        if (p + i < P) k[i] = keys[p + i];
+        if (p + i < P) k[i] = keys[p + i] & kM;
     }
     uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, k[3], 1);
     uint32_t next = __shfl_down_sync(0xFFFFFFFFu, k[0], 1);
-    if (lane == 0) prev = p > 0 && p - 1 < P ? keys[p - 1] : 0xFFFFFFFEu;
-    if (lane == 31) next = p + 4 < P ? keys[p + 4] : 0xFFFFFFFEu;
+    if (lane == 0) prev = p > 0 && p - 1 < P ? keys[p - 1] & kM : 0xFFFFFFFEu;
+    if (lane == 31) next = p + 4 < P ? keys[p + 4] & kM : 0xFFFFFFFEu;
     if (p >= P) continue;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {

@@ -147,6 +147,7 @@ live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alph
 // ---- row form of the exact tile test (R14 / N7), one row of one splat per item
 struct WarpRows {
   float u[32], v[32], B[32], det[32], ey[32], bs[32], at[32], invA[32], xr_ext[32], xl_ext[32];
+  int gx0[32], gx1[32], gy0[32], gy1[32];     // blend blocks (8x4 px, image-global) the splat's box meets
   int tx0[32], tx1[32], ty0[32];
   uint32_t excl[32], cnt[32], kb[32];
 };
@@ -189,8 +190,9 @@ __device__ __forceinline__ void row_cols(float xl, float xr, int tx0, int tx1, i
 // Rows of the 32 lanes' candidate boxes walked as one list; each row's kept
 // columns are appended to the kept-tile list (row-major per splat, splats in
 // lane order) at positions from a warp scan of the row counts.
-__device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, uint32_t kb,
-                                                   int width, int height, int TW, uint32_t *list, uint32_t list_cap,
+__device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, float rx, float ry,
+                                                   uint32_t kb, int width, int height, int TW, uint32_t *list,
+                                                   uint32_t list_cap,
                                                    uint32_t *list_top, uint32_t *overflow, uint32_t &list_off) {
   const uint32_t lane = lane_id(), lt = lanemask_lt();
   const int tx0 = (int)(o.box_x & 0xFFFFu), tx1 = (int)(o.box_x >> 16);
@@ -222,6 +224,16 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
     const float sD = __fsqrt_rn(D), Bb = __fmul_rn(o.B, bs);
     ws.xr_ext[lane] = __fadd_rn(o.u, __fmul_rn(__fsub_rn(sD, __fmul_rn(o.B, -bs)), invA));
     ws.xl_ext[lane] = __fsub_rn(o.u, __fmul_rn(__fadd_rn(sD, Bb), invA));
+    // blend.cu's block test for the 8x4 block (bx, by): u + rx >= 8 bx + 0.5, u - rx <= 8 bx + 7.5,
+    // v + ry >= 4 by + 0.5, v - ry <= 4 by + 3.5 (pixel centres).  Its solutions are the ranges
+    // [gx0, gx1] x [gy0, gy1] below, exactly: as in row_cols, each subtraction is exact wherever the
+    // rounding could matter (Sterbenz / ulp <= 0.5) and the scalings are by powers of two.
+    const float ux0 = __fsub_rn(o.u, rx), ux1 = __fadd_rn(o.u, rx);
+    const float vy0 = __fsub_rn(o.v, ry), vy1 = __fadd_rn(o.v, ry);
+    ws.gx1[lane] = (int)fminf(floorf(__fmul_rn(__fsub_rn(ux1, 0.5f), 0.125f)), 65536.0f);
+    ws.gx0[lane] = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(ux0, 7.5f), 0.125f)), -1.0f);
+    ws.gy1[lane] = (int)fminf(floorf(__fmul_rn(__fsub_rn(vy1, 0.5f), 0.25f)), 65536.0f);
+    ws.gy0[lane] = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(vy0, 3.5f), 0.25f)), -1.0f);
   }
   ws.tx0[lane] = tx0; ws.tx1[lane] = tx1; ws.ty0[lane] = ty0;
   __syncwarp();
@@ -256,9 +268,24 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
     if (n) {
       atomicAdd(&ws.cnt[owner], n);
       const uint32_t key0 = ws.kb[owner] + (uint32_t)(ty * TW);
+      // blend block mask (key bits 24..31): bit 2k + j <=> the splat's box {power >= skip bound}
+      // (u -/+ rx, v -/+ ry) meets the pixel centres of the 8x4 block (columns 8j.., rows 4k..) of the
+      // tile -- the same fp32 test blend.cu would run (N5)
+      // block rows k = 0..3 of tile row ty that the box meets -> bit pairs 2k, 2k+1
+      const int klo = max(ws.gy0[owner] - 4 * ty, 0), khi = min(ws.gy1[owner] - 4 * ty, 3);
+      const uint32_t ym = khi >= klo ? (4u << (2 * khi)) - (1u << (2 * klo)) : 0u;
+      // block columns j = 0, 1 of tile column tx that the box meets: both for the interior columns of
+      // [a, b] (the box spans them), so only the row's first and last column need the test
+      const int gx0 = ws.gx0[owner], gx1 = ws.gx1[owner];
+      auto colmask = [&](int tx) -> uint32_t {
+        const uint32_t xm = (gx0 <= 2 * tx && 2 * tx <= gx1 ? 1u : 0u) | (gx0 <= 2 * tx + 1 && 2 * tx + 1 <= gx1 ? 2u : 0u);
+        return (ym & (xm * 0x55u)) << 24;
+      };
+      const uint32_t ma = colmask(a), mb = colmask(b), mi = ym << 24;
       uint32_t pos = run + ex - n;
+#pragma unroll 1
       for (int tx = a; tx <= b; ++tx, ++pos)
-        if (pos < list_cap) list[pos] = key0 + (uint32_t)tx;
+        if (pos < list_cap) list[pos] = (key0 + (uint32_t)tx) | (tx == a ? ma : tx == b ? mb : mi);
     }
     run += step_tot;
   }
@@ -314,25 +341,28 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const SplatOut &o = so[e];
+      // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure; (rx, ry) =
+      // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel outside them
+      // has power < pmin, so the blend may skip it without changing a decision
+      float pmin = 0.0f, rx = 0.0f, ry = 0.0f;
+      if (ok[e]) {
+        pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+        const float qmax = __fmul_rn(-2.0f, pmin);
+        rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
+        ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
+      }
       uint32_t loff = 0;
-      const uint32_t n = warp_rows_list(ws, ok[e], o, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height, fc.TW,
-                                        sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
+      const uint32_t n = warp_rows_list(ws, ok[e], o, rx, ry, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
+                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
       if (!valid) continue;
       const uint32_t c = (uint32_t)e * n_live + i;
       uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
       if (ok[e]) {
         // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
-        // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure
-        const float pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
         dk = __float_as_uint(o.depth);
         sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
         sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
         sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-        // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel
-        // outside them has power < pmin, so the blend may skip it without changing a decision
-        const float qmax = __fmul_rn(-2.0f, pmin);
-        const float rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
-        const float ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
         sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
         sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
       } else {
