@@ -30,9 +30,10 @@ void launch_derive(const float pu[3], const uint32_t *, const float4 *, const in
 void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, uint32_t *, const SplatBufs &,
                     uint32_t *, FrameCounters *, int, cudaStream_t);
 int project_tile_size();
-void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, const uint32_t *,
+void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, int, const uint32_t *,
                      uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
-void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, cudaStream_t);
+void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, int,
+                 cudaStream_t);
 void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
                   const float4 *,
@@ -433,16 +434,19 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
                  reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
   mark();
   // a5 (depth digits of the (tile, depth) sort)
-  launch_onesweep(ctx->dkey_a.p, ctx->dval_a.p, ctx->dkey_b.p, ctx->dval_b.p, true, &ctr->n_splat, 4,
+  launch_onesweep(ctx->dkey_a.p, ctx->dval_a.p, ctx->dkey_b.p, ctx->dval_b.p, true, &ctr->n_splat, 4, 8,
                   &ctr->hist_depth[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[0],
                   ctx->num_sms, st);
   mark();
+  // the tile keys (eye * T_e + tile) take 2 passes of 7-bit digits when they fit in 14 bits (1080p:
+  // 2 T_e = 16320), else of 8-bit digits: 128 bins scatter in longer runs than 256
+  const int tbits = 2 * fc.Te <= (1 << 14) ? 7 : 8;
   EmitIn ei{ctx->dval_a.p, ctx->count.p, ctx->list_off.p, ctx->list.p, ctx->pair_off.p};
   launch_emit(ei, (uint32_t)ctx->cap_pairs, ctx->pkey_a.p, ctx->pval_a.p,
-              reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_emit), ctr, ctx->num_sms, st);
+              reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_emit), ctr, tbits, ctx->num_sms, st);
   mark();
   // a6 (tile digits)
-  launch_onesweep(ctx->pkey_a.p, ctx->pval_a.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2,
+  launch_onesweep(ctx->pkey_a.p, ctx->pval_a.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2, tbits,
                   &ctr->hist_tile[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[4],
                   ctx->num_sms, st);
   mark();

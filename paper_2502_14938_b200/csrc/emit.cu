@@ -105,7 +105,8 @@ __device__ __forceinline__ uint32_t warp_find(const uint32_t *__restrict__ pair_
 
 __global__ void __launch_bounds__(kXThreads)
 expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-              FrameCounters *__restrict__ ctr) {
+              FrameCounters *__restrict__ ctr, uint32_t tbits) {
+  const uint32_t tmask = (1u << tbits) - 1u;
   __shared__ uint32_t s_hist[2][256];
   for (int k = threadIdx.x; k < 512; k += kXThreads) (&s_hist[0][0])[k] = 0;
   __syncthreads();
@@ -129,8 +130,8 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
       const uint32_t key = in.list[in.list_off[c] + (q - in.pair_off[lo])];
       keys_out[q] = key;
       vals_out[q] = c;
-      atomicAdd(&s_hist[0][key & 0xFFu], 1u);
-      atomicAdd(&s_hist[1][(key >> 8) & 0xFFu], 1u);
+      atomicAdd(&s_hist[0][key & tmask], 1u);          // the tile sort's two tbits-bit digits
+      atomicAdd(&s_hist[1][(key >> tbits) & tmask], 1u);
     }
   }
   __syncthreads();
@@ -181,7 +182,7 @@ __global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCoun
 static int g_off_grid = 0, g_exp_grid = 0;
 
 void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *vals_out, uint32_t *status,
-                 FrameCounters *ctr, int num_sms, cudaStream_t st) {
+                 FrameCounters *ctr, int tbits, int num_sms, cudaStream_t st) {
   if (!g_off_grid) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_kernel, kXThreads, 0);
@@ -190,7 +191,7 @@ void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *v
     g_exp_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
   pairoff_kernel<<<g_off_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
-  expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr);
+  expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr, (uint32_t)tbits);
 }
 
 void launch_ranges(const uint32_t *keys, const FrameCounters *ctr, uint2 *ranges, int num_sms, cudaStream_t st) {

@@ -43,7 +43,8 @@ template <bool kIota>
 __global__ void __launch_bounds__(kSThreads, 4)
 onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
                      uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
-                     const uint32_t *__restrict__ d_count, uint32_t shift, const uint32_t *__restrict__ hist,
+                     const uint32_t *__restrict__ d_count, uint32_t shift, uint32_t dmask,
+                     const uint32_t *__restrict__ hist,
                      uint32_t *__restrict__ status, uint32_t *__restrict__ status_clear,
                      uint32_t *__restrict__ tile_ctr) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -89,7 +90,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
 #pragma unroll
     for (int i = 0; i < kSItems; ++i) {
       uint32_t idx = wbase + i * 32 + lane;
-      uint32_t d = idx < n ? (key[i] >> shift) & 0xFFu : (uint32_t)kBins;
+      uint32_t d = idx < n ? (key[i] >> shift) & dmask : (uint32_t)kBins;
       // peers = lanes holding the same digit: OR the lane bits into a per-digit shared word
       // (faster than match.any.sync here), then the lowest peer updates the count and clears it
       atomicOr(&S.match[warp][d], 1u << lane);
@@ -165,7 +166,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
     for (int i = 0; i < kSItems; ++i) {
       uint32_t idx = wbase + i * 32 + lane;
       if (idx < n) {
-        uint32_t d = (key[i] >> shift) & 0xFFu;
+        uint32_t d = (key[i] >> shift) & dmask;
         uint32_t pos = S.blk_off[d] + S.whist[warp][d] + rank[i];
         S.keys[pos] = key[i];
         S.vals[pos] = kIota ? idx : vals_in[idx];
@@ -175,7 +176,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
     const uint32_t nvalid = min((uint32_t)kSTile, n - tile * kSTile);
     for (uint32_t i = t; i < nvalid; i += kSThreads) {
       uint32_t k = S.keys[i];
-      uint32_t d = (k >> shift) & 0xFFu;
+      uint32_t d = (k >> shift) & dmask;
       uint32_t o = S.gbase[d] + (i - S.blk_off[d]);
       keys_out[o] = k;
       vals_out[o] = S.vals[i];
@@ -196,24 +197,26 @@ static void sort_setup(int num_sms) {
   g_sort_grid = num_sms * (per_sm > 0 ? per_sm : 1);
 }
 
-// Sort `passes` (even) 8-bit digits (shift 0, 8, ...) of keys_a[0..*d_count)
-// with payloads vals_a (iota payloads when `iota`).  Ping-pongs a -> b -> a;
+// Sort `passes` (even) digits of `bits` bits each (shift 0, bits, 2 bits, ...; bits <= 8) of
+// keys_a[0..*d_count) with payloads vals_a (iota payloads when `iota`).  Ping-pongs a -> b -> a;
 // with an even pass count the result lands back in keys_a / vals_a.
 void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, bool iota,
-                     const uint32_t *d_count, int passes, const uint32_t *hist /* [passes][256] */,
+                     const uint32_t *d_count, int passes, int bits, const uint32_t *hist /* [passes][256] */,
                      uint32_t *status_a, uint32_t *status_b, uint32_t *tile_ctrs, int num_sms, cudaStream_t st) {
   sort_setup(num_sms);
   const int smem = (int)sizeof(SortSmem);
+  const uint32_t dmask = (1u << bits) - 1u;
   for (int p = 0; p < passes; ++p) {
     const bool odd = p & 1;
     uint32_t *ki = odd ? keys_b : keys_a, *vi = odd ? vals_b : vals_a;
     uint32_t *ko = odd ? keys_a : keys_b, *vo = odd ? vals_a : vals_b;
     uint32_t *stc = odd ? status_b : status_a, *stx = odd ? status_a : status_b;
+    const uint32_t shift = (uint32_t)(bits * p);
     if (p == 0 && iota)
-      onesweep_pass_kernel<true><<<g_sort_grid, kSThreads, smem, st>>>(ki, nullptr, ko, vo, d_count, 8u * p,
+      onesweep_pass_kernel<true><<<g_sort_grid, kSThreads, smem, st>>>(ki, nullptr, ko, vo, d_count, shift, dmask,
                                                                         hist + 256 * p, stc, stx, tile_ctrs + p);
     else
-      onesweep_pass_kernel<false><<<g_sort_grid, kSThreads, smem, st>>>(ki, vi, ko, vo, d_count, 8u * p,
+      onesweep_pass_kernel<false><<<g_sort_grid, kSThreads, smem, st>>>(ki, vi, ko, vo, d_count, shift, dmask,
                                                                          hist + 256 * p, stc, stx, tile_ctrs + p);
   }
 }
