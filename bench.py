@@ -132,7 +132,7 @@ def run_gsc(args):
     traj = sg.trajectory(cfg)
     fmt = gp.GSC_FMT_RGBA8
     r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
-                    flags=gp.GSC_F_STAGE_TIMING, pair_capacity=args.pair_capacity).load(sc)
+                    flags=0, pair_capacity=args.pair_capacity).load(sc)
     out_l, out_r = r.alloc_outputs(fmt)
     stream = torch.cuda.current_stream(dev)
     frames = multi.frame_block(rank, world, len(traj), args.steps)
@@ -174,25 +174,31 @@ def run_gsc(args):
     multi.barrier()
     e2e_max = multi.max_over_ranks(t1 - t0, None if share else dev)
 
-    # blend evaluation counts for the roofline: an untimed replay of the same frames with counting on
-    # (counting costs blend instructions, so the timed runs above leave it off)
-    r.reset_cache()
-    r.set_flags(gp.GSC_F_COUNT_EVALS)
-    r.stats_history()
-    for f in frames:
-        r.render_into(traj[f], out_l, out_r, fmt, stream)
-    torch.cuda.synchronize()
-    counted = r.stats_history(max(args.steps, 1))
+    # per-stage times: a replay of the same frames with stage events and the front end / blend overlap
+    # of consecutive frames switched off (GSC_F_SERIAL), so the stage times add up to the frame time;
+    # then the blend evaluation counts for the roofline (counting costs blend instructions, so neither
+    # timed run counts)
+    def replay(flags):
+        r.reset_cache()
+        r.set_flags(flags)
+        r.stats_history()
+        for f in frames:
+            r.render_into(traj[f], out_l, out_r, fmt, stream)
+        torch.cuda.synchronize()
+        return r.stats_history(max(args.steps, 1))
+    staged = replay(gp.GSC_F_STAGE_TIMING | gp.GSC_F_SERIAL)
+    counted = replay(gp.GSC_F_COUNT_EVALS)
+    r.set_flags(0)
 
     total_frames = world * len(frames)
     value = total_frames / (t_max / 1000.0) if t_max > 0 else 0.0
 
     # per-stage measured ms (CUDA events inside the timed region) and roofline
     stages = ["cull", "derive", "project", "depth_sort", "emit", "tile_sort", "ranges", "blend"]
-    ms = {s: sum(h["ms_" + s] for h in hist) for s in stages}
-    nf = max(1, len(hist))
+    ms = {s: sum(h["ms_" + s] for h in staged) for s in stages}
+    nf = max(1, len(staged))
     algo = {s: 0.0 for s in stages}
-    for h in hist:
+    for h in staged:
         b = _stage_bytes(h, sc.n, 10, cfg.width, cfg.height, 4)
         for s in stages:
             algo[s] += b[s]
@@ -250,6 +256,9 @@ def run_gsc(args):
                        "l2": "no flush: per-frame working set (pool/splat/pair traffic ~1-2 GB) > 126 MB L2",
                        "parallelism": f"frames partitioned by view, scene replicated, dp{world}"},
             "stages": stage_report,
+            "stages_note": "CUDA events per stage in a replay of the same frames with GSC_F_SERIAL (no overlap of "
+                           "frame f+1's front end with frame f's blend); the timed run overlaps them on two streams",
+            "serial_ms_per_frame": round(sum(h["ms_total"] for h in staged) / nf, 4),
             "frame_counts": {"visible": round(sum(h["n_visible"] for h in hist) / nf),
                              "misses": round(sum(h["n_misses"] for h in hist) / nf),
                              "splats": round(sum(h["n_splats"] for h in hist) / nf),

@@ -63,6 +63,8 @@ typedef struct gsc_ctx gsc_ctx;
 #define GSC_F_DERIVE_CUDA_CORES 0x4u /* derivation MLP on CUDA cores (dp4a) instead of tcgen05 tensor cores */
 #define GSC_F_COUNT_EVALS 0x8u   /* blend counts its evaluations (gsc_frame_stats.n_evals / n_exp; else 0);
                                     costs blend time, so bench.py counts in a separate untimed pass */
+#define GSC_F_SERIAL 0x10u       /* do not overlap frame f+1's front end (cull .. ranges) with frame f's
+                                    blend: per-stage times then add up to the frame time */
 
 typedef struct {
   int width, height;        /* pixels per eye */

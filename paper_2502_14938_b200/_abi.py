@@ -21,6 +21,7 @@ GSC_F_DEPTH_LITERAL = 0x1
 GSC_F_STAGE_TIMING = 0x2
 GSC_F_DERIVE_CUDA_CORES = 0x4
 GSC_F_COUNT_EVALS = 0x8
+GSC_F_SERIAL = 0x10
 GSC_FMT_RGB_F32_PLANAR = 0
 GSC_FMT_RGBA8 = 1
 DBG = {"visible": 1, "misses": 2, "pool": 3, "splats": 4, "splat_g": 5, "pairs": 6, "pair_g": 7, "ranges": 8,

@@ -96,14 +96,23 @@ struct gsc_ctx {
   // per frame
   DevBuf<uint32_t> visible, misses;
   size_t cap_splat = 0, cap_pairs = 0;
-  DevBuf<float4> spA, spB, spC;
+  // What the blend of frame f reads lives in fs[f & 1]: the next frame's front end (cull .. ranges,
+  // stream sA) runs while this frame's blend (stream sB) still reads its set (inter-frame pipeline).
+  struct FrameSet {
+    DevBuf<float4> spA, spB, spC;
+    DevBuf<uint32_t> pkey, pval;           // tile-sorted pairs
+    DevBuf<uint2> ranges;
+    DevBuf<unsigned char> zero_region;     // FrameCounters | cull status | project status | emit status
+    FrameCounters *ctr() { return reinterpret_cast<FrameCounters *>(zero_region.p); }
+  } fs[2];
+  cudaStream_t sA = nullptr, sB = nullptr;
+  cudaEvent_t ev_user[2] = {nullptr, nullptr}, ev_a[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr};
+  bool b_pending[2] = {false, false};
   DevBuf<float2> spD;
   DevBuf<uint2> box;
   DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list, live_g;
-  DevBuf<uint32_t> pkey_a, pval_a, pkey_b, pval_b;
-  DevBuf<uint2> ranges;
+  DevBuf<uint32_t> pkey_b, pval_b;         // tile-sort scratch (front end only)
   DevBuf<uint32_t> sort_status_a, sort_status_b;
-  DevBuf<unsigned char> zero_region;     // FrameCounters | cull status | project status | emit status
   size_t zero_bytes = 0, off_cull = 0, off_proj = 0, off_emit = 0;
   DevBuf<FrameRecordDev> rec_dev;
   FrameRecordDev *rec_host = nullptr;    // pinned ring
@@ -116,7 +125,7 @@ struct gsc_ctx {
   // e2e staging
   DevBuf<unsigned char> img_dev[2];
 
-  FrameCounters *ctr() { return reinterpret_cast<FrameCounters *>(zero_region.p); }
+  FrameSet &last_set() { return fs[(frames_rendered + 1) & 1]; }   // the set of the last rendered frame
 };
 
 static gsc_status fail(gsc_ctx *c, gsc_status s, const std::string &msg) {
@@ -297,9 +306,11 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->visible.alloc(N));
   CU(ctx->misses.alloc(N));
   ctx->cap_splat = 2 * NK;
-  CU(ctx->spA.alloc(ctx->cap_splat));
-  CU(ctx->spB.alloc(ctx->cap_splat));
-  CU(ctx->spC.alloc(ctx->cap_splat));
+  for (auto &S : ctx->fs) {
+    CU(S.spA.alloc(ctx->cap_splat));
+    CU(S.spB.alloc(ctx->cap_splat));
+    CU(S.spC.alloc(ctx->cap_splat));
+  }
   CU(ctx->spD.alloc(ctx->cap_splat));
   CU(ctx->box.alloc(ctx->cap_splat));
   CU(ctx->count.alloc(ctx->cap_splat));
@@ -315,12 +326,14 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->list_off.alloc(ctx->cap_splat));
   CU(ctx->pair_off.alloc(ctx->cap_splat));
   CU(ctx->list.alloc(std::min<size_t>(2 * ctx->cap_pairs, (1u << 31) - 1)));
-  CU(ctx->pkey_a.alloc(ctx->cap_pairs));
-  CU(ctx->pval_a.alloc(ctx->cap_pairs));
   CU(ctx->pkey_b.alloc(ctx->cap_pairs));
   CU(ctx->pval_b.alloc(ctx->cap_pairs));
   const int TW = (ctx->cfg.width + 15) / 16, TH = (ctx->cfg.height + 15) / 16;
-  CU(ctx->ranges.alloc(2 * (size_t)TW * TH));
+  for (auto &S : ctx->fs) {
+    CU(S.pkey.alloc(ctx->cap_pairs));
+    CU(S.pval.alloc(ctx->cap_pairs));
+    CU(S.ranges.alloc(2 * (size_t)TW * TH));
+  }
   const size_t stiles = (std::max(ctx->cap_splat, ctx->cap_pairs) + sort_tile_size() - 1) / sort_tile_size();
   CU(ctx->sort_status_a.alloc(stiles * 256));
   CU(ctx->sort_status_b.alloc(stiles * 256));
@@ -331,8 +344,10 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   ctx->off_proj = ctx->off_cull + al((size_t)cull_tiles(N) * 8);
   ctx->off_emit = ctx->off_proj + al((ctx->cap_splat / 2 + project_tile_size() - 1) / project_tile_size() * 4);
   ctx->zero_bytes = ctx->off_emit + al((ctx->cap_splat + emit_tile_size() - 1) / emit_tile_size() * 4);
-  CU(ctx->zero_region.alloc(ctx->zero_bytes));
-  CU(cudaMemset(ctx->zero_region.p, 0, ctx->zero_bytes));
+  for (auto &S : ctx->fs) {
+    CU(S.zero_region.alloc(ctx->zero_bytes));
+    CU(cudaMemset(S.zero_region.p, 0, ctx->zero_bytes));
+  }
   CU(cudaDeviceSynchronize());
   ctx->have_scene = true;
   return reset_cache(ctx, nullptr);
@@ -395,71 +410,102 @@ static gsc_status load_file(gsc_ctx *ctx, const char *path) {
 }
 
 // ----------------------------------------------------------------------------------- frame
+static gsc_status ensure_streams(gsc_ctx *ctx) {
+  if (ctx->sA) return GSC_OK;
+  // (stream priorities were measured to make no difference: the two stages share every SM)
+  CU(cudaStreamCreateWithFlags(&ctx->sA, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ctx->sB, cudaStreamNonBlocking));
+  for (int k = 0; k < 2; ++k) {
+    CU(cudaEventCreateWithFlags(&ctx->ev_user[k], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->ev_a[k], cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->ev_b[k], cudaEventDisableTiming));
+  }
+  return GSC_OK;
+}
+
+// One frame = front end a1..a7 on stream sA, then blend a8 on stream sB, into frame set f & 1.  The
+// caller's stream `st` orders only the output images: the blend waits for the caller's earlier work
+// on `st`, and `st` waits for the blend.  Frame f+1's front end thus overlaps frame f's blend; it
+// waits for the blend of frame f-1, the last reader of the set it overwrites.
 static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaStream_t st) {
   if (ctx->sticky) return fail(ctx, GSC_ECUDA, "context has a sticky CUDA error: " + ctx->err);
   if (!ctx->have_scene || !ctx->have_pose) return fail(ctx, GSC_ESTATE, "render before load_scene/set_pose");
   if (!out_l || !out_r || (fmt != GSC_FMT_RGB_F32_PLANAR && fmt != GSC_FMT_RGBA8))
     return fail(ctx, GSC_EINVAL, "bad output buffers or format");
+  if (ensure_streams(ctx) != GSC_OK) return GSC_ECUDA;
   ctx->last_stream = st;
   const int slot_i = (int)(ctx->frames_rendered % kRing);
+  const int k = (int)(ctx->frames_rendered & 1);
+  auto &S = ctx->fs[k];
+  // GSC_F_SERIAL: one internal stream, so consecutive frames do not overlap (stage times add up)
+  cudaStream_t sA = ctx->sA, sB = (ctx->cfg.flags & GSC_F_SERIAL) ? ctx->sA : ctx->sB;
   FrameSlot &slot = ctx->slots[slot_i];
   const bool timed = (ctx->cfg.flags & GSC_F_STAGE_TIMING) != 0;
   if (timed && !slot.timed) {
-    for (int k = 0; k < kEvents; ++k) CU(cudaEventCreate(&slot.ev[k]));
+    for (int e = 0; e < kEvents; ++e) CU(cudaEventCreate(&slot.ev[e]));
     slot.timed = true;
   }
   int evk = 0;
-  auto mark = [&]() { if (timed) cudaEventRecord(slot.ev[evk++], st); };
-  FrameCounters *ctr = ctx->ctr();
+  auto mark = [&](cudaStream_t s) { if (timed) cudaEventRecord(slot.ev[evk++], s); };
+  CU(cudaEventRecord(ctx->ev_user[k], st));
+  if (ctx->b_pending[k]) CU(cudaStreamWaitEvent(sA, ctx->ev_b[k], 0));   // blend f-2 done with set k
+  FrameCounters *ctr = S.ctr();
   const FrameC &fc = ctx->fc;
-  mark();
-  CU(cudaMemsetAsync(ctx->zero_region.p, 0, ctx->zero_bytes, st));
-  CU(cudaMemsetAsync(ctx->ranges.p, 0, ctx->ranges.n * sizeof(uint2), st));
+  mark(sA);
+  CU(cudaMemsetAsync(S.zero_region.p, 0, ctx->zero_bytes, sA));
+  CU(cudaMemsetAsync(S.ranges.p, 0, S.ranges.n * sizeof(uint2), sA));
   const int cur = ctx->vis_cur;
   // a1 + a2
   launch_cull(fc, ctx->N, ctx->pos_m.p, ctx->level.p, ctx->birth.p, ctx->vis[cur ^ 1].p, ctx->vis[cur].p,
-              ctx->visible.p, ctx->misses.p, reinterpret_cast<unsigned long long *>(ctx->zero_region.p + ctx->off_cull),
-              ctr, ctx->policy.p, st);
-  launch_policy(ctx->policy.p, ctr, ctx->rec_dev.p + slot_i, st);
-  mark();
+              ctx->visible.p, ctx->misses.p, reinterpret_cast<unsigned long long *>(S.zero_region.p + ctx->off_cull),
+              ctr, ctx->policy.p, sA);
+  launch_policy(ctx->policy.p, ctr, ctx->rec_dev.p + slot_i, sA);
+  mark(sA);
   // a3
   launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p, ctx->b1s.p,
                 ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms,
-                (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, st);
-  mark();
+                (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, sA);
+  mark(sA);
   // a4
-  SplatBufs sb{ctx->spA.p, ctx->spB.p, ctx->spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
+  SplatBufs sb{S.spA.p, S.spB.p, S.spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
                ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
   launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, ctx->live_g.p, sb,
-                 reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_proj), ctr, ctx->num_sms, st);
-  mark();
+                 reinterpret_cast<uint32_t *>(S.zero_region.p + ctx->off_proj), ctr, ctx->num_sms, sA);
+  mark(sA);
   // a5 (depth digits of the (tile, depth) sort)
   launch_onesweep(ctx->dkey_a.p, ctx->dval_a.p, ctx->dkey_b.p, ctx->dval_b.p, true, &ctr->n_splat, 4, 8,
                   &ctr->hist_depth[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[0],
-                  ctx->num_sms, st);
-  mark();
+                  ctx->num_sms, sA);
+  mark(sA);
   // the tile keys (eye * T_e + tile) take 2 passes of 7-bit digits when they fit in 14 bits (1080p:
   // 2 T_e = 16320), else of 8-bit digits: 128 bins scatter in longer runs than 256
   const int tbits = 2 * fc.Te <= (1 << 14) ? 7 : 8;
   EmitIn ei{ctx->dval_a.p, ctx->count.p, ctx->list_off.p, ctx->list.p, ctx->pair_off.p};
-  launch_emit(ei, (uint32_t)ctx->cap_pairs, ctx->pkey_a.p, ctx->pval_a.p,
-              reinterpret_cast<uint32_t *>(ctx->zero_region.p + ctx->off_emit), ctr, tbits, ctx->num_sms, st);
-  mark();
+  launch_emit(ei, (uint32_t)ctx->cap_pairs, S.pkey.p, S.pval.p,
+              reinterpret_cast<uint32_t *>(S.zero_region.p + ctx->off_emit), ctr, tbits, ctx->num_sms, sA);
+  mark(sA);
   // a6 (tile digits)
-  launch_onesweep(ctx->pkey_a.p, ctx->pval_a.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2, tbits,
+  launch_onesweep(S.pkey.p, S.pval.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2, tbits,
                   &ctr->hist_tile[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[4],
-                  ctx->num_sms, st);
-  mark();
+                  ctx->num_sms, sA);
+  mark(sA);
   // a7
-  launch_ranges(ctx->pkey_a.p, ctr, ctx->ranges.p, ctx->num_sms, st);
-  mark();
-  // a8
-  launch_blend(fc, ctx->ranges.p, ctx->pkey_a.p, ctx->pval_a.p, ctx->spA.p, ctx->spB.p, ctx->spC.p, out_l, out_r, fmt, ctr,
-               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, st);
-  launch_record(ctr, ctx->rec_dev.p + slot_i, st);
+  launch_ranges(S.pkey.p, ctr, S.ranges.p, ctx->num_sms, sA);
+  mark(sA);
+  CU(cudaEventRecord(ctx->ev_a[k], sA));
+  // a8 on sB, after the front end and after the caller's earlier work on its stream
+  CU(cudaStreamWaitEvent(sB, ctx->ev_a[k], 0));
+  CU(cudaStreamWaitEvent(sB, ctx->ev_user[k], 0));
+  mark(sB);
+  launch_blend(fc, S.ranges.p, S.pkey.p, S.pval.p, S.spA.p, S.spB.p, S.spC.p, out_l, out_r, fmt, ctr,
+               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, sB);
+  launch_record(ctr, ctx->rec_dev.p + slot_i, sB);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
-                     st));
-  mark();
+                     sB));
+  mark(sB);
+  CU(cudaEventRecord(ctx->ev_b[k], sB));
+  ctx->b_pending[k] = true;
+  CU(cudaStreamWaitEvent(st, ctx->ev_b[k], 0));
   CU(cudaGetLastError());
   slot.used = true;
   ctx->vis_cur ^= 1;
@@ -487,11 +533,15 @@ static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
   s->novelty_rate = r.n_visible ? (float)r.n_new / (float)r.n_visible : 0.0f;
   FrameSlot &slot = ctx->slots[slot_i];
   if (slot.timed && (ctx->cfg.flags & GSC_F_STAGE_TIMING)) {
+    // ev 0..7 on the front-end stream, ev 8..9 around the blend on the blend stream (the blend of
+    // frame f overlaps the front end of frame f+1, so the stage times may sum to more than the
+    // frame period)
     float ms[8] = {0};
-    for (int k = 0; k < 8; ++k) cudaEventElapsedTime(&ms[k], slot.ev[k], slot.ev[k + 1]);
+    for (int k = 0; k < 7; ++k) cudaEventElapsedTime(&ms[k], slot.ev[k], slot.ev[k + 1]);
+    cudaEventElapsedTime(&ms[7], slot.ev[8], slot.ev[9]);
     s->ms_cull = ms[0]; s->ms_derive = ms[1]; s->ms_project = ms[2]; s->ms_depth_sort = ms[3];
     s->ms_emit = ms[4]; s->ms_tile_sort = ms[5]; s->ms_ranges = ms[6]; s->ms_blend = ms[7];
-    cudaEventElapsedTime(&s->ms_total, slot.ev[0], slot.ev[8]);
+    cudaEventElapsedTime(&s->ms_total, slot.ev[0], slot.ev[9]);
     (void)cudaGetLastError();   // an event query must not leave a sticky error behind
   }
 }
@@ -581,6 +631,8 @@ gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream) {
   CU(cudaSetDevice(ctx->device));
   CU(cudaStreamSynchronize((cudaStream_t)cuda_stream));
   if (ctx->own_stream) CU(cudaStreamSynchronize(ctx->own_stream));
+  if (ctx->sA) CU(cudaStreamSynchronize(ctx->sA));
+  if (ctx->sB) CU(cudaStreamSynchronize(ctx->sB));
   return GSC_OK;
 }
 
@@ -604,7 +656,8 @@ gsc_status gsc_reset_cache(gsc_ctx *ctx) {
 
 gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
   if (!ctx) return GSC_EINVAL;
-  const unsigned known = GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS;
+  const unsigned known =
+      GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL;
   if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
   CU(cudaSetDevice(ctx->device));
   CU(cudaDeviceSynchronize());
@@ -617,8 +670,9 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
   CU(cudaSetDevice(ctx->device));
   CU(cudaDeviceSynchronize());
   if (!ctx->have_scene || ctx->frames_rendered == 0) return fail(ctx, GSC_ESTATE, "no frame rendered");
+  auto &S = ctx->last_set();
   FrameCounters c;
-  CU(cudaMemcpy(&c, ctx->zero_region.p, sizeof(c), cudaMemcpyDeviceToHost));
+  CU(cudaMemcpy(&c, S.zero_region.p, sizeof(c), cudaMemcpyDeviceToHost));
   const size_t NK = (size_t)ctx->N * kK;
   const size_t ns = c.n_splat, np = c.n_pairs;
   auto copy_dev = [&](const void *src, size_t bytes) -> gsc_status {
@@ -635,7 +689,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       *len = np * 4;
       if (!host_dst || !cap) return GSC_OK;
       std::vector<uint32_t> pv(np), gs(ns);
-      CU(cudaMemcpy(pv.data(), ctx->pval_a.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(pv.data(), S.pval.p, np * 4, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(gs.data(), ctx->gslot.p, ns * 4, cudaMemcpyDeviceToHost));
       std::vector<uint32_t> out(np);
       for (size_t k = 0; k < np; ++k) out[k] = gs[pv[k]];
@@ -647,8 +701,8 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       if (!host_dst || !cap) return GSC_OK;
       std::vector<uint32_t> pk(np), pv(np);
       std::vector<float2> D(ns);
-      CU(cudaMemcpy(pk.data(), ctx->pkey_a.p, np * 4, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(pv.data(), ctx->pval_a.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(pk.data(), S.pkey.p, np * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(pv.data(), S.pval.p, np * 4, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
       std::vector<uint64_t> out(np);
       for (size_t k = 0; k < np; ++k) {
@@ -659,7 +713,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
       return GSC_OK;
     }
-    case GSC_DBG_RANGES: return copy_dev(ctx->ranges.p, ctx->ranges.n * 8);
+    case GSC_DBG_RANGES: return copy_dev(S.ranges.p, S.ranges.n * 8);
     case GSC_DBG_POOL: {
       *len = NK * 13 * 4;
       if (!host_dst || !cap) return GSC_OK;
@@ -683,9 +737,9 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       std::vector<float2> D(ns);
       std::vector<uint2> bx(ns);
       std::vector<uint32_t> cn(ns);
-      CU(cudaMemcpy(A.data(), ctx->spA.p, ns * 16, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(B.data(), ctx->spB.p, ns * 16, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(Cc.data(), ctx->spC.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(A.data(), S.spA.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(B.data(), S.spB.p, ns * 16, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(Cc.data(), S.spC.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(bx.data(), ctx->box.p, ns * 8, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(cn.data(), ctx->count.p, ns * 4, cudaMemcpyDeviceToHost));
@@ -724,6 +778,13 @@ void gsc_destroy(gsc_ctx *ctx) {
       for (int k = 0; k < kEvents; ++k) cudaEventDestroy(s.ev[k]);
   if (ctx->rec_host) cudaFreeHost(ctx->rec_host);
   if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+  for (int k = 0; k < 2; ++k) {
+    if (ctx->ev_user[k]) cudaEventDestroy(ctx->ev_user[k]);
+    if (ctx->ev_a[k]) cudaEventDestroy(ctx->ev_a[k]);
+    if (ctx->ev_b[k]) cudaEventDestroy(ctx->ev_b[k]);
+  }
+  if (ctx->sA) cudaStreamDestroy(ctx->sA);
+  if (ctx->sB) cudaStreamDestroy(ctx->sB);
   delete ctx;
 }
 
