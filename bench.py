@@ -163,13 +163,21 @@ def run_gsc(args):
     overflow = any(h["overflow"] for h in hist)
 
     # end-to-end through the public API: host pose in, RGBA8 images into pinned host memory
+    # (asynchronous API: frame f's image copy overlaps frame f+1's computation; two host image pairs,
+    # every frame's images have landed in host memory before the clock stops)
     r.reset_cache()
-    hl = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
-    hr = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
+    host = [(torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory(),
+             torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()) for _ in range(2)]
     multi.barrier()
     t0 = time.perf_counter()
-    for f in frames:
-        r.render_host(traj[f], hl, hr, fmt)
+    seqs = []
+    for j, f in enumerate(frames):
+        if j >= 2:
+            r.wait_frame(seqs[j - 2])          # host pair j % 2 is free again
+        hl, hr = host[j % 2]
+        seqs.append(r.render_host_async(traj[f], hl, hr, fmt))
+    for q in seqs[-2:]:
+        r.wait_frame(q)
     t1 = time.perf_counter()
     multi.barrier()
     e2e_max = multi.max_over_ranks(t1 - t0, None if share else dev)

@@ -160,6 +160,20 @@ gsc_status gsc_render_pair(gsc_ctx *ctx, void *out_left, void *out_right, int ou
 gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
                                 int out_format, gsc_frame_stats *stats);
 
+/* Asynchronous end-to-end call: set the pose, enqueue the frame and the copy
+ * of its two images into caller-owned HOST buffers (pinned, or the copy is
+ * synchronous), and return without waiting.  *seq receives the frame's
+ * sequence number.  The host buffers must stay valid and unread until
+ * gsc_wait_frame(ctx, *seq) returns; frames complete in submission order, so
+ * frame f's copy overlaps frame f+1's computation.  GSC_EINVAL on NULL
+ * arguments or a bad format. */
+gsc_status gsc_render_pair_host_async(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
+                                      int out_format, long long *seq);
+
+/* Block until frame `seq` (from gsc_render_pair_host_async) has landed in
+ * its host buffers.  GSC_EINVAL for a sequence number not yet submitted. */
+gsc_status gsc_wait_frame(gsc_ctx *ctx, long long seq);
+
 /* Wait for the context's outstanding work on `cuda_stream`. */
 gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream);
 

@@ -116,6 +116,20 @@ class Renderer:
         self._chk(_abi.lib().gsc_render_pair_host(self.h, C.byref(r), C.c_void_p(host_l.data_ptr()),
                                                   C.c_void_p(host_r.data_ptr()), fmt, None))
 
+    def render_host_async(self, rig, host_l, host_r, fmt: int = GSC_FMT_RGBA8) -> int:
+        """Asynchronous end-to-end call: enqueue the frame and the copy of its images into host (pinned)
+        tensors; returns the frame's sequence number for wait_frame.  Keep the tensors untouched until
+        then (frame f's copy overlaps frame f+1's computation)."""
+        import ctypes as C
+        r = _abi.make_rig(rig)
+        seq = C.c_longlong()
+        self._chk(_abi.lib().gsc_render_pair_host_async(self.h, C.byref(r), C.c_void_p(host_l.data_ptr()),
+                                                        C.c_void_p(host_r.data_ptr()), fmt, C.byref(seq)))
+        return seq.value
+
+    def wait_frame(self, seq: int):
+        self._chk(_abi.lib().gsc_wait_frame(self.h, seq))
+
     def sync(self, stream=None):
         import ctypes as C
         self._chk(_abi.lib().gsc_sync(self.h, C.c_void_p(stream.cuda_stream if stream is not None else 0)))

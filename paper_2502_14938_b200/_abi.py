@@ -75,6 +75,9 @@ _SIGS = {
                                   C.POINTER(gsc_frame_stats)]),
     "gsc_render_pair_host": (C.c_int, [C.c_void_p, C.POINTER(gsc_rig), C.c_void_p, C.c_void_p, C.c_int,
                                        C.POINTER(gsc_frame_stats)]),
+    "gsc_render_pair_host_async": (C.c_int, [C.c_void_p, C.POINTER(gsc_rig), C.c_void_p, C.c_void_p, C.c_int,
+                                             C.POINTER(C.c_longlong)]),
+    "gsc_wait_frame": (C.c_int, [C.c_void_p, C.c_longlong]),
     "gsc_sync": (C.c_int, [C.c_void_p, C.c_void_p]),
     "gsc_stats_history": (C.c_int, [C.c_void_p, C.POINTER(gsc_frame_stats), C.c_int, C.POINTER(C.c_int)]),
     "gsc_reset_cache": (C.c_int, [C.c_void_p]),

@@ -122,8 +122,11 @@ struct gsc_ctx {
   float pu[3] = {0, 0, 0};
   cudaStream_t last_stream = nullptr;
   cudaStream_t own_stream = nullptr;
-  // e2e staging
-  DevBuf<unsigned char> img_dev[2];
+  // e2e staging: device images per frame parity (the copy of frame f overlaps the blend of frame f+1)
+  DevBuf<unsigned char> img_dev[2][2];
+  static constexpr int kHostRing = 8;
+  cudaEvent_t host_done[kHostRing] = {};
+  int64_t host_submitted = 0;
 
   FrameSet &last_set() { return fs[(frames_rendered + 1) & 1]; }   // the set of the last rendered frame
 };
@@ -604,25 +607,62 @@ gsc_status gsc_render_pair(gsc_ctx *ctx, void *out_left, void *out_right, int ou
   return GSC_OK;
 }
 
-gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right, int out_format,
-                                gsc_frame_stats *stats) {
-  if (!ctx || !rig || !host_left || !host_right) return GSC_EINVAL;
-  CU(cudaSetDevice(ctx->device));
+// enqueue: pose, frame into the device staging images of its parity, D2H copies; all on own_stream
+static gsc_status render_host_enqueue(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
+                                      int out_format) {
+  if (out_format != GSC_FMT_RGB_F32_PLANAR && out_format != GSC_FMT_RGBA8) return GSC_EINVAL;
   gsc_status s = gsc_set_pose(ctx, rig);
   if (s != GSC_OK) return s;
   if (!ctx->own_stream) CU(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   const size_t bytes = (size_t)ctx->cfg.width * ctx->cfg.height * (out_format == GSC_FMT_RGBA8 ? 4 : 12);
+  auto &img = ctx->img_dev[ctx->frames_rendered & 1];
   for (int e = 0; e < 2; ++e)
-    if (ctx->img_dev[e].n < bytes) CU(ctx->img_dev[e].alloc(bytes));
-  s = render(ctx, ctx->img_dev[0].p, ctx->img_dev[1].p, out_format, ctx->own_stream);
+    if (img[e].n < bytes) {
+      CU(cudaDeviceSynchronize());   // (re)allocation only when the format grows
+      CU(img[e].alloc(bytes));
+    }
+  s = render(ctx, img[0].p, img[1].p, out_format, ctx->own_stream);
   if (s != GSC_OK) return s;
-  CU(cudaMemcpyAsync(host_left, ctx->img_dev[0].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
-  CU(cudaMemcpyAsync(host_right, ctx->img_dev[1].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
+  CU(cudaMemcpyAsync(host_left, img[0].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
+  CU(cudaMemcpyAsync(host_right, img[1].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
+  return GSC_OK;
+}
+
+gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right, int out_format,
+                                gsc_frame_stats *stats) {
+  if (!ctx || !rig || !host_left || !host_right) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  gsc_status s = render_host_enqueue(ctx, rig, host_left, host_right, out_format);
+  if (s != GSC_OK) return s;
   CU(cudaStreamSynchronize(ctx->own_stream));
   if (stats) {
     fill_stats(ctx, ctx->frames_rendered - 1, stats);
     if (stats->overflow) return fail(ctx, GSC_ECAPACITY, "pair capacity exceeded");
   }
+  return GSC_OK;
+}
+
+gsc_status gsc_render_pair_host_async(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
+                                      int out_format, long long *seq) {
+  if (!ctx || !rig || !host_left || !host_right || !seq) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  const int64_t q = ctx->host_submitted;
+  auto &ev = ctx->host_done[q % gsc_ctx::kHostRing];
+  if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  else CU(cudaEventSynchronize(ev));   // the ring slot's previous frame (kHostRing in flight at most)
+  gsc_status s = render_host_enqueue(ctx, rig, host_left, host_right, out_format);
+  if (s != GSC_OK) return s;
+  CU(cudaEventRecord(ev, ctx->own_stream));
+  *seq = q;
+  ++ctx->host_submitted;
+  return GSC_OK;
+}
+
+gsc_status gsc_wait_frame(gsc_ctx *ctx, long long seq) {
+  if (!ctx || seq < 0 || seq >= ctx->host_submitted) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  if (seq + gsc_ctx::kHostRing <= ctx->host_submitted) return GSC_OK;   // its slot was already waited for
+  CU(cudaEventSynchronize(ctx->host_done[seq % gsc_ctx::kHostRing]));
   return GSC_OK;
 }
 
@@ -783,6 +823,8 @@ void gsc_destroy(gsc_ctx *ctx) {
     if (ctx->ev_a[k]) cudaEventDestroy(ctx->ev_a[k]);
     if (ctx->ev_b[k]) cudaEventDestroy(ctx->ev_b[k]);
   }
+  for (auto &e : ctx->host_done)
+    if (e) cudaEventDestroy(e);
   if (ctx->sA) cudaStreamDestroy(ctx->sA);
   if (ctx->sB) cudaStreamDestroy(ctx->sB);
   delete ctx;
