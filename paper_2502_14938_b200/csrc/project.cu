@@ -144,32 +144,78 @@ live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alph
   }
 }
 
-// ---- row form of the exact tile test (R14 / N7), one row of one splat per item
+// ---- row form of the exact tile test (R14 / N7)
+// Per-splat constants of the row walk.
+struct RowSplat {
+  float u, v, B, det, ey, bs, at, invA, xr_ext, xl_ext;
+  int gx0, gx1, gy0, gy1;   // blend blocks (8x4 px, image-global) the splat's skip box meets
+  int tx0, tx1, ty0;
+  uint32_t kb;              // key base of the eye (eye * T_e)
+};
+
+__device__ __forceinline__ RowSplat row_splat(const SplatOut &o, float rx, float ry, uint32_t kb) {
+  RowSplat r;
+  const float det = __fsub_rn(__fmul_rn(o.A, o.C), __fmul_rn(o.B, o.B));
+  const float bs = __fmul_rn(o.B, __fsqrt_rn(__fdiv_rn(o.thr, __fmul_rn(det, o.C))));
+  const float at = __fmul_rn(o.A, o.thr), invA = __fdiv_rn(1.0f, o.A);
+  r.u = o.u; r.v = o.v; r.B = o.B; r.det = det; r.at = at; r.invA = invA; r.bs = bs;
+  r.ey = __fsqrt_rn(__fmul_rn(o.thr, __fdiv_rn(o.A, det)));
+  // the rows' x-extremes when no clamp is active (dyr = -bs, dyl = bs), same expression as row_interval
+  const float D = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(bs, bs))), 0.0f);
+  const float sD = __fsqrt_rn(D), Bb = __fmul_rn(o.B, bs);
+  r.xr_ext = __fadd_rn(o.u, __fmul_rn(__fsub_rn(sD, __fmul_rn(o.B, -bs)), invA));
+  r.xl_ext = __fsub_rn(o.u, __fmul_rn(__fadd_rn(sD, Bb), invA));
+  // blend.cu's block test for the 8x4 block (bx, by): u + rx >= 8 bx + 0.5, u - rx <= 8 bx + 7.5,
+  // v + ry >= 4 by + 0.5, v - ry <= 4 by + 3.5 (pixel centres).  Its solutions are the ranges
+  // [gx0, gx1] x [gy0, gy1] below, exactly: as in row_cols, each subtraction is exact wherever the
+  // rounding could matter (Sterbenz / ulp <= 0.5) and the scalings are by powers of two.
+  const float ux0 = __fsub_rn(o.u, rx), ux1 = __fadd_rn(o.u, rx);
+  const float vy0 = __fsub_rn(o.v, ry), vy1 = __fadd_rn(o.v, ry);
+  r.gx1 = (int)fminf(floorf(__fmul_rn(__fsub_rn(ux1, 0.5f), 0.125f)), 65536.0f);
+  r.gx0 = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(ux0, 7.5f), 0.125f)), -1.0f);
+  r.gy1 = (int)fminf(floorf(__fmul_rn(__fsub_rn(vy1, 0.5f), 0.25f)), 65536.0f);
+  r.gy0 = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(vy0, 3.5f), 0.25f)), -1.0f);
+  r.tx0 = (int)(o.box_x & 0xFFFFu); r.tx1 = (int)(o.box_x >> 16);
+  r.ty0 = (int)(o.box_y & 0xFFFFu);
+  r.kb = kb;
+  return r;
+}
+
+// the cooperative walk's shared copy of the 32 lanes' RowSplats (SoA)
 struct WarpRows {
   float u[32], v[32], B[32], det[32], ey[32], bs[32], at[32], invA[32], xr_ext[32], xl_ext[32];
-  int gx0[32], gx1[32], gy0[32], gy1[32];     // blend blocks (8x4 px, image-global) the splat's box meets
-  int tx0[32], tx1[32], ty0[32];
-  uint32_t excl[32], cnt[32], kb[32];
+  int gx0[32], gx1[32], gy0[32], gy1[32], tx0[32], tx1[32], ty0[32];
+  uint32_t kb[32], excl[32], cnt[32];
+  __device__ __forceinline__ void put(int l, const RowSplat &r) {
+    u[l] = r.u; v[l] = r.v; B[l] = r.B; det[l] = r.det; ey[l] = r.ey; bs[l] = r.bs; at[l] = r.at;
+    invA[l] = r.invA; xr_ext[l] = r.xr_ext; xl_ext[l] = r.xl_ext; gx0[l] = r.gx0; gx1[l] = r.gx1;
+    gy0[l] = r.gy0; gy1[l] = r.gy1; tx0[l] = r.tx0; tx1[l] = r.tx1; ty0[l] = r.ty0; kb[l] = r.kb;
+  }
+  __device__ __forceinline__ RowSplat get(int l) const {
+    RowSplat r;
+    r.u = u[l]; r.v = v[l]; r.B = B[l]; r.det = det[l]; r.ey = ey[l]; r.bs = bs[l]; r.at = at[l];
+    r.invA = invA[l]; r.xr_ext = xr_ext[l]; r.xl_ext = xl_ext[l]; r.gx0 = gx0[l]; r.gx1 = gx1[l];
+    r.gy0 = gy0[l]; r.gy1 = gy1[l]; r.tx0 = tx0[l]; r.tx1 = tx1[l]; r.ty0 = ty0[l]; r.kb = kb[l];
+    return r;
+  }
 };
 
 // x-interval [xl, xr] of the ellipse {q <= thr} over the pixel-centre rows of tile row ty.  When the
 // band contains the extreme rows dy = -/+ B s (the usual case) the clamps are inactive and the per-row
 // expression equals the per-splat xr_ext / xl_ext bit for bit.
-__device__ __forceinline__ bool row_interval(const WarpRows &ws, int o, int ty, int height, float &xl, float &xr) {
-  const float ey = ws.ey[o], bs = ws.bs[o], v = ws.v[o];
+__device__ __forceinline__ bool row_interval(const RowSplat &r, int ty, int height, float &xl, float &xr) {
   const int py1 = min(16 * ty + 15, height - 1);
   const float Y0 = __fadd_rn((float)(16 * ty), 0.5f), Y1 = __fadd_rn((float)py1, 0.5f);
-  const float lo = fmaxf(__fsub_rn(Y0, v), -ey), hi = fminf(__fsub_rn(Y1, v), ey);
+  const float lo = fmaxf(__fsub_rn(Y0, r.v), -r.ey), hi = fminf(__fsub_rn(Y1, r.v), r.ey);
   if (!(lo <= hi)) return false;
-  const float dyr = fminf(fmaxf(-bs, lo), hi), dyl = fminf(fmaxf(bs, lo), hi);
-  xr = ws.xr_ext[o];
-  xl = ws.xl_ext[o];
-  if (dyr != -bs || dyl != bs) {
-    const float u = ws.u[o], B = ws.B[o], det = ws.det[o], at = ws.at[o], invA = ws.invA[o];
-    const float Dr = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyr, dyr))), 0.0f);
-    xr = __fadd_rn(u, __fmul_rn(__fsub_rn(__fsqrt_rn(Dr), __fmul_rn(B, dyr)), invA));
-    const float Dl = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(dyl, dyl))), 0.0f);
-    xl = __fsub_rn(u, __fmul_rn(__fadd_rn(__fsqrt_rn(Dl), __fmul_rn(B, dyl)), invA));
+  const float dyr = fminf(fmaxf(-r.bs, lo), hi), dyl = fminf(fmaxf(r.bs, lo), hi);
+  xr = r.xr_ext;
+  xl = r.xl_ext;
+  if (dyr != -r.bs || dyl != r.bs) {
+    const float Dr = fmaxf(__fsub_rn(r.at, __fmul_rn(r.det, __fmul_rn(dyr, dyr))), 0.0f);
+    xr = __fadd_rn(r.u, __fmul_rn(__fsub_rn(__fsqrt_rn(Dr), __fmul_rn(r.B, dyr)), r.invA));
+    const float Dl = fmaxf(__fsub_rn(r.at, __fmul_rn(r.det, __fmul_rn(dyl, dyl))), 0.0f);
+    xl = __fsub_rn(r.u, __fmul_rn(__fadd_rn(__fsqrt_rn(Dl), __fmul_rn(r.B, dyl)), r.invA));
   }
   return true;
 }
@@ -187,119 +233,130 @@ __device__ __forceinline__ void row_cols(float xl, float xr, int tx0, int tx1, i
   if (a <= b && __fadd_rn((float)min(16 * a + 15, width - 1), 0.5f) < xl) ++a;
 }
 
-// Rows of the 32 lanes' candidate boxes walked as one list; each row's kept
-// columns are appended to the kept-tile list (row-major per splat, splats in
-// lane order) at positions from a warp scan of the row counts.
+// kept columns [a, b] of row ty as keys (bits 0..23: eye * T_e + ty TW + tx) with the blend block mask
+// (bits 24..31): bit 2k + j <=> the splat's skip box (u -/+ rx, v -/+ ry) meets the pixel centres of
+// the tile's 8x4 block at columns 8j.., rows 4k.. -- the fp32 test blend.cu would run (N5).
+__device__ __forceinline__ void emit_row(const RowSplat &r, int ty, int a, int b, int TW, uint32_t *list,
+                                         uint32_t list_cap, uint32_t pos) {
+  const uint32_t key0 = r.kb + (uint32_t)(ty * TW);
+  // block rows k = 0..3 of tile row ty that the box meets -> bit pairs 2k, 2k+1
+  const int klo = max(r.gy0 - 4 * ty, 0), khi = min(r.gy1 - 4 * ty, 3);
+  const uint32_t ym = khi >= klo ? (4u << (2 * khi)) - (1u << (2 * klo)) : 0u;
+  // block columns j = 0, 1 of tile column tx: both for the interior columns of [a, b] (the box spans
+  // them), so only the row's first and last column need the test
+  auto colmask = [&](int tx) -> uint32_t {
+    const uint32_t xm = (r.gx0 <= 2 * tx && 2 * tx <= r.gx1 ? 1u : 0u) |
+                        (r.gx0 <= 2 * tx + 1 && 2 * tx + 1 <= r.gx1 ? 2u : 0u);
+    return (ym & (xm * 0x55u)) << 24;
+  };
+  const uint32_t ma = colmask(a), mb = colmask(b), mi = ym << 24;
+#pragma unroll 1
+  for (int tx = a; tx <= b; ++tx, ++pos)
+    if (pos < list_cap) list[pos] = (key0 + (uint32_t)tx) | (tx == a ? ma : tx == b ? mb : mi);
+}
+
+constexpr uint32_t kSmallRows = 3;   // boxes of <= 3 tile rows: walked by their own lane
+
+// Kept tiles of the 32 lanes' splats.  The warp bump-allocates the sum of the candidate box areas (an
+// upper bound) from the kept-tile list.  A splat whose box has <= kSmallRows rows is walked by its own
+// lane (row by row) into its own area; the rest -- the heavy tail of near, large splats -- are walked
+// cooperatively: their rows laid end to end, 32 rows per step (one per lane), kept keys packed.
 __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, float rx, float ry,
                                                    uint32_t kb, int width, int height, int TW, uint32_t *list,
-                                                   uint32_t list_cap,
-                                                   uint32_t *list_top, uint32_t *overflow, uint32_t &list_off) {
-  const uint32_t lane = lane_id(), lt = lanemask_lt();
-  const int tx0 = (int)(o.box_x & 0xFFFFu), tx1 = (int)(o.box_x >> 16);
-  const int ty0 = (int)(o.box_y & 0xFFFFu), ty1 = (int)((o.box_y >> 16) & 0x7FFFu);
-  const uint32_t nrows = has ? (uint32_t)(ty1 - ty0 + 1) : 0u;
-  const uint32_t area = has ? nrows * (uint32_t)(tx1 - tx0 + 1) : 0u;
-  uint32_t inc = nrows, tot_area = area;
+                                                   uint32_t list_cap, uint32_t *list_top, uint32_t *overflow,
+                                                   uint32_t &list_off) {
+  const uint32_t lane = lane_id();
+  RowSplat r{};
+  uint32_t nrows = 0, area = 0;
+  if (has) {
+    r = row_splat(o, rx, ry, kb);
+    nrows = (uint32_t)((int)((o.box_y >> 16) & 0x7FFFu) - r.ty0 + 1);
+    area = nrows * (uint32_t)(r.tx1 - r.tx0 + 1);
+  }
+  const bool small = has && nrows <= kSmallRows, big = has && !small;
+  // exclusive scans: small areas (own regions), big rows (cooperative items); totals
+  uint32_t s_inc = small ? area : 0u, b_rows = big ? nrows : 0u, b_area = big ? area : 0u;
 #pragma unroll
   for (int off = 1; off < 32; off <<= 1) {
-    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, off);
-    if (lane >= (uint32_t)off) inc += t;
+    const uint32_t t1 = __shfl_up_sync(0xFFFFFFFFu, s_inc, off), t2 = __shfl_up_sync(0xFFFFFFFFu, b_rows, off);
+    if (lane >= (uint32_t)off) { s_inc += t1; b_rows += t2; }
   }
 #pragma unroll
-  for (int off = 16; off > 0; off >>= 1) tot_area += __shfl_xor_sync(0xFFFFFFFFu, tot_area, off);
-  const uint32_t total = __shfl_sync(0xFFFFFFFFu, inc, 31);
-  ws.excl[lane] = inc - nrows;
-  ws.cnt[lane] = 0;
-  ws.kb[lane] = kb;
-  if (has) {
-    const float det = __fsub_rn(__fmul_rn(o.A, o.C), __fmul_rn(o.B, o.B));
-    const float bs = __fmul_rn(o.B, __fsqrt_rn(__fdiv_rn(o.thr, __fmul_rn(det, o.C))));
-    const float at = __fmul_rn(o.A, o.thr), invA = __fdiv_rn(1.0f, o.A);
-    ws.u[lane] = o.u; ws.v[lane] = o.v; ws.B[lane] = o.B; ws.det[lane] = det; ws.at[lane] = at;
-    ws.invA[lane] = invA;
-    ws.ey[lane] = __fsqrt_rn(__fmul_rn(o.thr, __fdiv_rn(o.A, det)));
-    ws.bs[lane] = bs;
-    // the rows' x-extremes when no clamp is active (dyr = -bs, dyl = bs), same expression as row_interval
-    const float D = fmaxf(__fsub_rn(at, __fmul_rn(det, __fmul_rn(bs, bs))), 0.0f);
-    const float sD = __fsqrt_rn(D), Bb = __fmul_rn(o.B, bs);
-    ws.xr_ext[lane] = __fadd_rn(o.u, __fmul_rn(__fsub_rn(sD, __fmul_rn(o.B, -bs)), invA));
-    ws.xl_ext[lane] = __fsub_rn(o.u, __fmul_rn(__fadd_rn(sD, Bb), invA));
-    // blend.cu's block test for the 8x4 block (bx, by): u + rx >= 8 bx + 0.5, u - rx <= 8 bx + 7.5,
-    // v + ry >= 4 by + 0.5, v - ry <= 4 by + 3.5 (pixel centres).  Its solutions are the ranges
-    // [gx0, gx1] x [gy0, gy1] below, exactly: as in row_cols, each subtraction is exact wherever the
-    // rounding could matter (Sterbenz / ulp <= 0.5) and the scalings are by powers of two.
-    const float ux0 = __fsub_rn(o.u, rx), ux1 = __fadd_rn(o.u, rx);
-    const float vy0 = __fsub_rn(o.v, ry), vy1 = __fadd_rn(o.v, ry);
-    ws.gx1[lane] = (int)fminf(floorf(__fmul_rn(__fsub_rn(ux1, 0.5f), 0.125f)), 65536.0f);
-    ws.gx0[lane] = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(ux0, 7.5f), 0.125f)), -1.0f);
-    ws.gy1[lane] = (int)fminf(floorf(__fmul_rn(__fsub_rn(vy1, 0.5f), 0.25f)), 65536.0f);
-    ws.gy0[lane] = (int)fmaxf(ceilf(__fmul_rn(__fsub_rn(vy0, 3.5f), 0.25f)), -1.0f);
-  }
-  ws.tx0[lane] = tx0; ws.tx1[lane] = tx1; ws.ty0[lane] = ty0;
-  __syncwarp();
+  for (int off = 16; off > 0; off >>= 1) b_area += __shfl_xor_sync(0xFFFFFFFFu, b_area, off);
+  const uint32_t s_tot = __shfl_sync(0xFFFFFFFFu, s_inc, 31), b_tot_rows = __shfl_sync(0xFFFFFFFFu, b_rows, 31);
   uint32_t base = 0;
   if (lane == 0) {
-    base = atomicAdd(list_top, tot_area);                   // upper bound: the boxes' areas
-    if (base + tot_area > list_cap || base + tot_area < base) atomicExch(overflow, 1u);
+    const uint32_t need = s_tot + b_area;
+    base = atomicAdd(list_top, need);
+    if (base + need > list_cap || base + need < base) atomicExch(overflow, 1u);
   }
   base = __shfl_sync(0xFFFFFFFFu, base, 0);
-  uint32_t run = base;
-  for (uint32_t w0 = 0; w0 < total; w0 += 32) {
-    const uint32_t w = w0 + lane;
-    int owner = 0, a = 0, b = -1, ty = 0;
-    if (w < total) {
-      int lo = 0;
-#pragma unroll
-      for (int step = 16; step > 0; step >>= 1)
-        if (ws.excl[lo + step] <= w) lo += step;
-      owner = lo;
-      ty = ws.ty0[lo] + (int)(w - ws.excl[lo]);
+  uint32_t n = 0;
+  if (small) {
+    const uint32_t pos0 = base + s_inc - area;
+    list_off = pos0;
+    for (uint32_t k = 0; k < nrows; ++k) {
+      const int ty = r.ty0 + (int)k;
       float xl, xr;
-      if (row_interval(ws, lo, ty, height, xl, xr)) row_cols(xl, xr, ws.tx0[lo], ws.tx1[lo], width, a, b);
+      int a = 0, b = -1;
+      if (row_interval(r, ty, height, xl, xr)) row_cols(xl, xr, r.tx0, r.tx1, width, a, b);
+      if (b >= a) {
+        emit_row(r, ty, a, b, TW, list, list_cap, pos0 + n);
+        n += (uint32_t)(b - a + 1);
+      }
     }
-    const uint32_t n = b >= a ? (uint32_t)(b - a + 1) : 0u;
-    uint32_t ex = n;
+  }
+  if (b_tot_rows) {   // warp-uniform
+    const uint32_t nb = big ? nrows : 0u;
+    ws.excl[lane] = b_rows - nb;
+    ws.cnt[lane] = 0;
+    if (big) ws.put(lane, r);
+    __syncwarp();
+    uint32_t run = base + s_tot;
+    for (uint32_t w0 = 0; w0 < b_tot_rows; w0 += 32) {
+      const uint32_t w = w0 + lane;
+      int owner = 0, a = 0, b = -1, ty = 0;
+      RowSplat q{};
+      if (w < b_tot_rows) {
+        int lo = 0;
+#pragma unroll
+        for (int step = 16; step > 0; step >>= 1)
+          if (ws.excl[lo + step] <= w) lo += step;
+        owner = lo;
+        q = ws.get(lo);
+        ty = q.ty0 + (int)(w - ws.excl[lo]);
+        float xl, xr;
+        if (row_interval(q, ty, height, xl, xr)) row_cols(xl, xr, q.tx0, q.tx1, width, a, b);
+      }
+      const uint32_t m = b >= a ? (uint32_t)(b - a + 1) : 0u;
+      uint32_t ex = m;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ex, off);
+        if (lane >= (uint32_t)off) ex += t;
+      }
+      const uint32_t step_tot = __shfl_sync(0xFFFFFFFFu, ex, 31);
+      if (m) {
+        atomicAdd(&ws.cnt[owner], m);
+        emit_row(q, ty, a, b, TW, list, list_cap, run + ex - m);
+      }
+      run += step_tot;
+    }
+    __syncwarp();
+    const uint32_t nbig = big ? ws.cnt[lane] : 0u;
+    uint32_t e2 = nbig;
 #pragma unroll
     for (int off = 1; off < 32; off <<= 1) {
-      uint32_t t = __shfl_up_sync(0xFFFFFFFFu, ex, off);
-      if (lane >= (uint32_t)off) ex += t;
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, e2, off);
+      if (lane >= (uint32_t)off) e2 += t;
     }
-    const uint32_t step_tot = __shfl_sync(0xFFFFFFFFu, ex, 31);
-    if (n) {
-      atomicAdd(&ws.cnt[owner], n);
-      const uint32_t key0 = ws.kb[owner] + (uint32_t)(ty * TW);
-      // blend block mask (key bits 24..31): bit 2k + j <=> the splat's box {power >= skip bound}
-      // (u -/+ rx, v -/+ ry) meets the pixel centres of the 8x4 block (columns 8j.., rows 4k..) of the
-      // tile -- the same fp32 test blend.cu would run (N5)
-      // block rows k = 0..3 of tile row ty that the box meets -> bit pairs 2k, 2k+1
-      const int klo = max(ws.gy0[owner] - 4 * ty, 0), khi = min(ws.gy1[owner] - 4 * ty, 3);
-      const uint32_t ym = khi >= klo ? (4u << (2 * khi)) - (1u << (2 * klo)) : 0u;
-      // block columns j = 0, 1 of tile column tx that the box meets: both for the interior columns of
-      // [a, b] (the box spans them), so only the row's first and last column need the test
-      const int gx0 = ws.gx0[owner], gx1 = ws.gx1[owner];
-      auto colmask = [&](int tx) -> uint32_t {
-        const uint32_t xm = (gx0 <= 2 * tx && 2 * tx <= gx1 ? 1u : 0u) | (gx0 <= 2 * tx + 1 && 2 * tx + 1 <= gx1 ? 2u : 0u);
-        return (ym & (xm * 0x55u)) << 24;
-      };
-      const uint32_t ma = colmask(a), mb = colmask(b), mi = ym << 24;
-      uint32_t pos = run + ex - n;
-#pragma unroll 1
-      for (int tx = a; tx <= b; ++tx, ++pos)
-        if (pos < list_cap) list[pos] = (key0 + (uint32_t)tx) | (tx == a ? ma : tx == b ? mb : mi);
+    if (big) {
+      n = nbig;
+      list_off = base + s_tot + e2 - nbig;
     }
-    run += step_tot;
+    __syncwarp();
   }
-  (void)lt;
-  __syncwarp();
-  const uint32_t n = has ? ws.cnt[lane] : 0u;
-  __syncwarp();
-  uint32_t e2 = n;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    uint32_t t = __shfl_up_sync(0xFFFFFFFFu, e2, off);
-    if (lane >= (uint32_t)off) e2 += t;
-  }
-  list_off = base + e2 - n;
+  if (!has) list_off = base;
   return n;
 }
 
