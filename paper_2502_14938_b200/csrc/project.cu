@@ -250,9 +250,14 @@ __device__ __forceinline__ void emit_row(const RowSplat &r, int ty, int a, int b
     return (ym & (xm * 0x55u)) << 24;
   };
   const uint32_t ma = colmask(a), mb = colmask(b), mi = ym << 24;
+  const uint32_t n = (uint32_t)(b - a + 1), key = key0 + (uint32_t)a;
+  if (pos + n <= list_cap && pos + n >= pos) {   // (else the overflow flag is already set)
+    uint32_t *dst = list + pos;
+    dst[0] = key | ma;
 #pragma unroll 1
-  for (int tx = a; tx <= b; ++tx, ++pos)
-    if (pos < list_cap) list[pos] = (key0 + (uint32_t)tx) | (tx == a ? ma : tx == b ? mb : mi);
+    for (uint32_t t = 1; t + 1 < n; ++t) dst[t] = (key + t) | mi;
+    if (n > 1) dst[n - 1] = (key + n - 1) | mb;
+  }
 }
 
 constexpr uint32_t kSmallRows = 3;   // boxes of <= 3 tile rows: walked by their own lane
