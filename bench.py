@@ -28,6 +28,8 @@ import sys
 import tempfile
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -242,6 +244,7 @@ def run_gsc(args):
         roof["traffic_source"] = tr[kernels[dom][0]]["source"]
     except (OSError, KeyError, ValueError):
         pass
+    ft = np.array([h["ms_total"] for h in staged], dtype=np.float64) if staged else np.zeros(1)
     stage_report = {s: {"ms_per_frame": round(ms[s] / nf, 4),
                         "GBps": round(algo[s] / (ms[s] / 1000.0) / 1e9, 1) if ms[s] > 0 else None}
                     for s in stages}
@@ -267,6 +270,10 @@ def run_gsc(args):
             "stages_note": "CUDA events per stage in a replay of the same frames with GSC_F_SERIAL (no overlap of "
                            "frame f+1's front end with frame f's blend); the timed run overlaps them on two streams",
             "serial_ms_per_frame": round(sum(h["ms_total"] for h in staged) / nf, 4),
+            # per-frame times of the serial replay ("99% FPS" = 1st percentile of per-frame FPS)
+            "frame_ms": {"mean": round(float(np.mean(ft)), 4), "p50": round(float(np.percentile(ft, 50)), 4),
+                         "p99": round(float(np.percentile(ft, 99)), 4), "max": round(float(np.max(ft)), 4),
+                         "fps_99pct": round(float(1000.0 / np.percentile(ft, 99)), 2)},
             "frame_counts": {"visible": round(sum(h["n_visible"] for h in hist) / nf),
                              "misses": round(sum(h["n_misses"] for h in hist) / nf),
                              "splats": round(sum(h["n_splats"] for h in hist) / nf),
