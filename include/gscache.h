@@ -63,6 +63,16 @@ typedef struct gsc_ctx gsc_ctx;
 #define GSC_F_DERIVE_CUDA_CORES 0x4u /* derivation MLP on CUDA cores (dp4a) instead of tcgen05 tensor cores */
 #define GSC_F_COUNT_EVALS 0x8u   /* blend counts its evaluations (gsc_frame_stats.n_evals / n_exp; else 0);
                                     costs blend time, so bench.py counts in a separate untimed pass */
+#define GSC_F_GUIDE_EXP 0x20u    /* guiding function H (Eq. 4): exponential response, depth = max(1, D_max >>
+                                    floor(4 rate)) ("exponential response"; R23) */
+#define GSC_F_GUIDE_STAGED 0x40u /* staged response: D_max / ceil(D_max/2) / ceil(D_max/4) / 1 for rate below
+                                    1/10 / 1/4 / 1/2 / above ("staged response"; R23).  Neither flag:
+                                    the linear H of the paper's experiments.  Take effect at gsc_reset_cache;
+                                    setting both is GSC_EINVAL */
+#define GSC_F_ABL_FIXED_EXTENT 0x80u /* ablation: tile extent r^2 = 9 (fixed 3 sigma) instead
+                                        of the opacity-aware 2 ln(255 alpha); the blend is unchanged */
+#define GSC_F_ABL_AABB_TILES 0x100u  /* ablation (F1): keep every tile of the candidate box (no exact tile test,
+                                        P:256) -- more pairs, same pixels */
 #define GSC_F_SERIAL 0x10u       /* do not overlap frame f+1's front end (cull .. ranges) with frame f's
                                     blend: per-stage times then add up to the frame time */
 

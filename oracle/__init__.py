@@ -63,7 +63,8 @@ class Scene(C.Structure):
 class Config(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("fov_y", C.c_double),
                 ("near_plane", C.c_double), ("far_plane", C.c_double), ("bg", C.c_float * 3),
-                ("d_max", C.c_int), ("depth_literal", C.c_int)]
+                ("d_max", C.c_int), ("depth_literal", C.c_int), ("guide", C.c_int),
+                ("ablate", C.c_int)]
 
 
 class Eye(C.Structure):
@@ -125,6 +126,7 @@ def lib():
         L.orc_blend_pixel.argtypes = [vp, i32, f32, f32, vp, vp, vp, vp]
         L.orc_blend_pixel.restype = None
         L.orc_depth_H.argtypes = [i32, C.c_int64, C.c_int64]
+        L.orc_depth_H_guide.argtypes = [i32, i32, C.c_int64, C.c_int64]
         L.orc_create.restype = vp
         L.orc_create.argtypes = [C.POINTER(Scene), C.POINTER(Config)]
         L.orc_destroy.argtypes = [vp]
@@ -162,7 +164,7 @@ def elem(fn: str, x) -> np.ndarray:
 
 
 def make_config(width, height, fov_y_deg=70.0, near=0.05, far=5000.0, d_max=10, bg=(0, 0, 0),
-                depth_literal=False) -> Config:
+                depth_literal=False, guide=0, ablate=0) -> Config:
     c = Config()
     c.width, c.height = width, height
     c.fov_y = np.deg2rad(fov_y_deg)
@@ -171,6 +173,8 @@ def make_config(width, height, fov_y_deg=70.0, near=0.05, far=5000.0, d_max=10, 
         c.bg[k] = bg[k]
     c.d_max = d_max
     c.depth_literal = int(depth_literal)
+    c.guide = int(guide)       # 0 linear, 1 exponential, 2 staged (R23)
+    c.ablate = int(ablate)     # ORC_ABL_* bits: 1 fixed 3-sigma extent, 2 AABB tiles (F1 ablations)
     return c
 
 

@@ -252,6 +252,26 @@ int orc_depth_H(int d_max, int64_t num, int64_t den) {
   return 1 + (int)((2 * (int64_t)(d_max - 1) * (den - num) + den) / (2 * den));
 }
 
+/* Guiding-function variants ("exponential response and staged response are needed" for
+ * accelerating / staged motion; the paper gives no formulas -- readings R23):
+ *   ORC_GUIDE_EXP:    depth = max(1, D >> floor(4 num/den))  (halve the depth per quarter of the rate)
+ *   ORC_GUIDE_STAGED: depth = D if rate < 1/10, ceil(D/2) if rate < 1/4, ceil(D/4) if rate < 1/2, else 1
+ * Both exact in integers; H(0) = D, H(1) = 1, monotone non-increasing like the linear one. */
+int orc_depth_H_guide(int guide, int d_max, int64_t num, int64_t den) {
+  if (guide == ORC_GUIDE_LINEAR) return orc_depth_H(d_max, num, den);
+  if (den <= 0) return d_max;
+  if (guide == ORC_GUIDE_EXP) {
+    int64_t q = (4 * num) / den;                 /* 0..4 */
+    int d = d_max >> (int)q;
+    return d < 1 ? 1 : d;
+  }
+  /* staged */
+  if (10 * num < den) return d_max;
+  if (4 * num < den) return (d_max + 1) / 2;
+  if (2 * num < den) return (d_max + 3) / 4;
+  return 1;
+}
+
 /* Eq. 2: Sigma = R S S^T R^T; q = raw (w,x,y,z) normalised (zero -> identity),
  * R by the 3DGS rotation formula, M = R diag(S), Sigma = M M^T (6 entries 00 01 02 11 12 22). */
 void orc_build_cov(const float qin[4], const float S[3], float cov[6]) {
@@ -374,6 +394,7 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
   o->u = (ec->fx * xz) + ec->cx;
   o->v = (ec->fy * yz) + ec->cy;
   float r2 = 2.0f * orc_log_s(rho);                         /* r^2 = 2 ln(alpha/eps) */
+  if (cfg->ablate & ORC_ABL_FIXED_EXTENT) r2 = 9.0f;        /* ablation: fixed 3 sigma */
   o->thr = (r2 * ORC_KAPPA) + ORC_SLACK;
   o->alpha = alpha;
   o->rgb[0] = rgb[0]; o->rgb[1] = rgb[1]; o->rgb[2] = rgb[2];
@@ -454,6 +475,7 @@ int orc_row_interval(const orc_config *cfg, const orc_splat *s, int ty, float *x
 }
 
 int orc_tile_kept(const orc_config *cfg, const orc_splat *s, int tx, int ty) {
+  if (cfg->ablate & ORC_ABL_AABB_TILES) return 1;           /* ablation: candidate box only */
   float xl, xr;
   if (!orc_row_interval(cfg, s, ty, &xl, &xr)) return 0;
   int px1 = 16 * tx + 15;
@@ -620,7 +642,7 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
   /* Alg. 1 l.198: depth <- H(rate); R10: rate = novelty |X_f \ X_f-1| / |X_f|
    * (SPEC-literal alternative: miss rate). Frame 0 keeps D_max. */
   int depth_next = depth;
-  if (f > 0) depth_next = orc_depth_H(cfg->d_max, cfg->depth_literal ? nm : nnew, nv);
+  if (f > 0) depth_next = orc_depth_H_guide(cfg->guide, cfg->d_max, cfg->depth_literal ? nm : nnew, nv);
   if (stats) {
     memset(stats, 0, sizeof(*stats));
     stats->frame = f;

@@ -52,7 +52,16 @@ typedef struct {
   float bg[3];
   int d_max;
   int depth_literal; /* 1: SPEC-literal H(miss rate); 0: H(novelty) */
+  int guide;         /* guiding function H: ORC_GUIDE_LINEAR (default), _EXP, _STAGED (R23) */
+  int ablate;        /* ORC_ABL_* bits (SURVEY §8(f) F1 ablations of P:256; 0 = the method) */
 } orc_config;
+
+#define ORC_ABL_FIXED_EXTENT 1  /* extent r^2 = 9 (fixed 3 sigma) instead of 2 ln(255 alpha) */
+#define ORC_ABL_AABB_TILES 2    /* every tile of the candidate box kept (no exact tile test) */
+
+#define ORC_GUIDE_LINEAR 0
+#define ORC_GUIDE_EXP 1
+#define ORC_GUIDE_STAGED 2
 
 typedef struct { double p[3]; double q[4]; } orc_eye;
 
@@ -107,6 +116,7 @@ float orc_tile_qmin(const orc_config *cfg, const orc_splat *s, int tx, int ty);
 void orc_blend_pixel(const orc_splat *const *list, int n, float px_center_x, float px_center_y,
                      const float bg[3], float out[3], float *T_out, int *n_eval);
 int orc_depth_H(int d_max, int64_t num, int64_t den);
+int orc_depth_H_guide(int guide, int d_max, int64_t num, int64_t den);
 
 /* ---- whole frames ---- */
 typedef struct orc_state orc_state;

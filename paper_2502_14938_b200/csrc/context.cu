@@ -147,7 +147,8 @@ static gsc_status fail(gsc_ctx *c, gsc_status s, const std::string &msg) {
 static bool cfg_valid(const gsc_config *c) {
   return c && c->width > 0 && c->height > 0 && c->width <= 16 * 65535 && c->fov_y > 0 && c->fov_y < M_PI &&
          c->near_plane > 0 && c->far_plane > c->near_plane && c->d_max >= 1 &&
-         2LL * ((c->width + 15) / 16) * ((c->height + 15) / 16) <= 65536;
+         2LL * ((c->width + 15) / 16) * ((c->height + 15) / 16) <= 65536 &&
+         !((c->flags & GSC_F_GUIDE_EXP) && (c->flags & GSC_F_GUIDE_STAGED));
 }
 
 // ----------------------------------------------------------------------------------- camera (a0)
@@ -368,6 +369,7 @@ static gsc_status reset_cache(gsc_ctx *ctx, cudaStream_t st) {
   ps.W = -ctx->cfg.d_max;                 // W_0 = 0 - depth_0
   ps.d_max = ctx->cfg.d_max;
   ps.literal = (ctx->cfg.flags & GSC_F_DEPTH_LITERAL) ? 1 : 0;
+  ps.guide = (ctx->cfg.flags & GSC_F_GUIDE_EXP) ? 1 : (ctx->cfg.flags & GSC_F_GUIDE_STAGED) ? 2 : 0;
   CU(cudaMemcpyAsync(ctx->policy.p, &ps, sizeof(ps), cudaMemcpyHostToDevice, st));
   CU(cudaStreamSynchronize(st));
   return GSC_OK;
@@ -453,6 +455,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   CU(cudaEventRecord(ctx->ev_user[k], st));
   if (ctx->b_pending[k]) CU(cudaStreamWaitEvent(sA, ctx->ev_b[k], 0));   // blend f-2 done with set k
   FrameCounters *ctr = S.ctr();
+  ctx->fc.ablate = ((ctx->cfg.flags & GSC_F_ABL_FIXED_EXTENT) ? kAblFixedExtent : 0) |
+                   ((ctx->cfg.flags & GSC_F_ABL_AABB_TILES) ? kAblAabbTiles : 0);
   const FrameC &fc = ctx->fc;
   mark(sA);
   CU(cudaMemsetAsync(S.zero_region.p, 0, ctx->zero_bytes, sA));
@@ -697,8 +701,10 @@ gsc_status gsc_reset_cache(gsc_ctx *ctx) {
 gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
   if (!ctx) return GSC_EINVAL;
   const unsigned known =
-      GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL;
+      GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL |
+      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES;
   if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
+  if ((flags & GSC_F_GUIDE_EXP) && (flags & GSC_F_GUIDE_STAGED)) return fail(ctx, GSC_EINVAL, "two guiding functions");
   CU(cudaSetDevice(ctx->device));
   CU(cudaDeviceSynchronize());
   ctx->cfg.flags = flags;

@@ -143,7 +143,18 @@ __global__ void policy_kernel(PolicyState *pol, const FrameCounters *ctr, FrameR
   const long long den = ctr->n_visible;
   const long long num = pol->literal ? (long long)ctr->n_miss : (long long)ctr->n_new;
   int32_t depth_next = depth_used;
-  if (f > 0) depth_next = den <= 0 ? D : 1 + (int32_t)((2LL * (D - 1) * (den - num) + den) / (2LL * den));
+  if (f > 0) {
+    if (den <= 0) {
+      depth_next = D;
+    } else if (pol->guide == 1) {           // exponential: halve the depth per quarter of the rate (R23)
+      const int32_t d = D >> (int32_t)((4LL * num) / den);
+      depth_next = d < 1 ? 1 : d;
+    } else if (pol->guide == 2) {           // staged: thresholds 1/10, 1/4, 1/2 (R23)
+      depth_next = 10LL * num < den ? D : 4LL * num < den ? (D + 1) / 2 : 2LL * num < den ? (D + 3) / 4 : 1;
+    } else {                                // linear: clamp(1 + round_half_away((D-1)(1-rate)), 1, D)
+      depth_next = 1 + (int32_t)((2LL * (D - 1) * (den - num) + den) / (2LL * den));
+    }
+  }
   pol->depth = depth_next;
   const int32_t wn = (f + 1) - depth_next;
   pol->W = pol->W > wn ? pol->W : wn;

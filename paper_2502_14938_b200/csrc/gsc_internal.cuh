@@ -31,7 +31,10 @@ struct FrameC {
   int L;
   float d0;
   float bg[3];
+  int ablate;   // kAbl* bits (GSC_F_ABL_*): F1 ablations of the extent / tile test
 };
+constexpr int kAblFixedExtent = 1;
+constexpr int kAblAabbTiles = 2;
 
 // ---- device-resident counters, zeroed at every frame start ----
 struct FrameCounters {
@@ -56,7 +59,8 @@ struct PolicyState {
   int32_t W;           // watermark W_f = max_{f'<=f}(f' - depth_f')
   int32_t d_max;
   int32_t literal;     // GSC_F_DEPTH_LITERAL
-  int32_t pad[3];
+  int32_t guide;       // guiding function: 0 linear, 1 exponential, 2 staged (GSC_F_GUIDE_*)
+  int32_t pad[2];
 };
 
 // compacted splat records (index c), written by project, read by emit/blend

@@ -25,13 +25,14 @@ constexpr int kLTile = kLThreads * kLRounds;      // 4096 slots per CTA tile
 
 struct SplatOut {
   float u, v, A, B, C, thr;
+  float r2s;               // 2 ln(255 alpha): the significance radius^2, whatever extent the tiles use
   float sxx, syy;          // 2D covariance diagonal (after the 0.3 floor)
   uint32_t box_x, box_y;   // tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
   uint32_t n;
   float depth;
 };
 
-__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float alpha,
+__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, int ablate, float alpha,
                                             const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
   float rho = __fmul_rn(255.0f, alpha);
   if (!(rho > 1.0f)) return false;
@@ -74,6 +75,8 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   o.u = __fadd_rn(__fmul_rn(ec.fx, xz), ec.cx);
   o.v = __fadd_rn(__fmul_rn(ec.fy, yz), ec.cy);
   float r2 = __fmul_rn(2.0f, log_s(rho));
+  o.r2s = r2;
+  if (ablate & kAblFixedExtent) r2 = 9.0f;   // ablation (GSC_F_ABL_FIXED_EXTENT): fixed 3 sigma
   o.thr = __fadd_rn(__fmul_rn(r2, kKappa), kSlack);
   o.depth = z;
   if (!isfinite(o.A) || !isfinite(o.B) || !isfinite(o.C) || !isfinite(o.u) || !isfinite(o.v) || !isfinite(o.thr))
@@ -269,7 +272,7 @@ constexpr uint32_t kSmallRows = 3;   // boxes of <= 3 tile rows: walked by their
 __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, float rx, float ry,
                                                    uint32_t kb, int width, int height, int TW, uint32_t *list,
                                                    uint32_t list_cap, uint32_t *list_top, uint32_t *overflow,
-                                                   uint32_t &list_off) {
+                                                   bool aabb, uint32_t &list_off) {
   const uint32_t lane = lane_id();
   RowSplat r{};
   uint32_t nrows = 0, area = 0;
@@ -304,7 +307,8 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
       const int ty = r.ty0 + (int)k;
       float xl, xr;
       int a = 0, b = -1;
-      if (row_interval(r, ty, height, xl, xr)) row_cols(xl, xr, r.tx0, r.tx1, width, a, b);
+      if (aabb) { a = r.tx0; b = r.tx1; }
+      else if (row_interval(r, ty, height, xl, xr)) row_cols(xl, xr, r.tx0, r.tx1, width, a, b);
       if (b >= a) {
         emit_row(r, ty, a, b, TW, list, list_cap, pos0 + n);
         n += (uint32_t)(b - a + 1);
@@ -331,7 +335,8 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
         q = ws.get(lo);
         ty = q.ty0 + (int)(w - ws.excl[lo]);
         float xl, xr;
-        if (row_interval(q, ty, height, xl, xr)) row_cols(xl, xr, q.tx0, q.tx1, width, a, b);
+        if (aabb) { a = q.tx0; b = q.tx1; }
+        else if (row_interval(q, ty, height, xl, xr)) row_cols(xl, xr, q.tx0, q.tx1, width, a, b);
       }
       const uint32_t m = b >= a ? (uint32_t)(b - a + 1) : 0u;
       uint32_t ex = m;
@@ -398,7 +403,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       q2 = pool[3 * (size_t)g + 2];
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        ok[e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, so[e]);
+        ok[e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, fc.ablate, al, q0, q1, q2, so[e]);
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -408,14 +413,15 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       // has power < pmin, so the blend may skip it without changing a decision
       float pmin = 0.0f, rx = 0.0f, ry = 0.0f;
       if (ok[e]) {
-        pmin = __fsub_rn(-__fmul_rn(0.5f, __fsub_rn(o.thr, kSlack) / kKappa), 0.0078125f);
+        pmin = __fsub_rn(__fmul_rn(-0.5f, o.r2s), 0.0078125f);
         const float qmax = __fmul_rn(-2.0f, pmin);
         rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
         ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
       }
       uint32_t loff = 0;
       const uint32_t n = warp_rows_list(ws, ok[e], o, rx, ry, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
-                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
+                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow,
+                                        (fc.ablate & kAblAabbTiles) != 0, loff);
       if (!valid) continue;
       const uint32_t c = (uint32_t)e * n_live + i;
       uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile

@@ -77,6 +77,42 @@ def test_c1_moving_trajectory_cache(orc, c1):
         _frame_parity(orc, o, r, rig)
 
 
+@pytest.mark.parametrize("guide", [1, 2])
+def test_c1_guide_variants(orc, c1, guide):
+    """Exponential / staged guiding functions (GSC_F_GUIDE_EXP / _STAGED, R23) over a moving
+    trajectory: depths, hit/miss sets every frame and full parity on some frames."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    flag = gp.GSC_F_GUIDE_EXP if guide == 1 else gp.GSC_F_GUIDE_STAGED
+    o = orc.Oracle(sc, oracle_config(orc, cfg, guide=guide))
+    r = renderer(cfg, flags=flag).load(sc)
+    c = cfg.center
+    depths = set()
+    for f in range(20):
+        # inside the block at eye height, the view direction jumping by 2.5 rad (x0.3 every other
+        # pair of frames): novelty 7-46%, so both guides leave D_max
+        eye = c + np.array([2.0 * np.cos(0.1 * f), 2.0 * np.sin(0.1 * f), 1.7])
+        a = 2.5 * f * (1.0 if f % 4 < 2 else 0.3)
+        rig = sg.look_at_rig(eye, eye + np.array([np.cos(a), np.sin(a), -0.1]), 0.064)
+        st, _ = _frame_parity(orc, o, r, rig, full=(f % 7 == 0))
+        depths.add(st["depth_next"])
+    assert len(depths) > 1
+
+
+@pytest.mark.parametrize("ablate", [1, 2, 3])
+def test_c1_ablations(orc, c1, ablate):
+    """F1 ablations (GSC_F_ABL_FIXED_EXTENT = 1, GSC_F_ABL_AABB_TILES = 2, both = 3) against the
+    oracle with the same ablation: every intermediate bit-exact on the four C1 poses."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    flags = (gp.GSC_F_ABL_FIXED_EXTENT if ablate & 1 else 0) | (gp.GSC_F_ABL_AABB_TILES if ablate & 2 else 0)
+    o = orc.Oracle(sc, oracle_config(orc, cfg, ablate=ablate))
+    r = renderer(cfg, flags=flags).load(sc)
+    for rig in sg.trajectory(cfg):
+        st, d = _frame_parity(orc, o, r, rig)
+        assert d == 0.0
+
+
 def test_c1_spec_literal_depth(orc, c1):
     import paper_2502_14938_b200 as gp
     cfg, sc = c1

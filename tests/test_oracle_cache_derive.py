@@ -33,6 +33,48 @@ def test_depth_H_endpoints_and_rounding(orc):
             assert all(a >= b for a, b in zip(vals, vals[1:]))  # monotone non-increasing
 
 
+def test_depth_H_guide_variants(orc):
+    """Exponential and staged guiding functions (reading R23): exact rational definitions,
+    endpoints H(0) = D_max and H(1) = 1, monotone non-increasing; guide 0 is the linear H."""
+    G = orc.lib().orc_depth_H_guide
+    for D in (1, 2, 5, 10, 17):
+        for den in (1, 3, 7, 100, 1001):
+            prev = {1: D, 2: D}
+            for num in range(den + 1):
+                r = Fraction(num, den)
+                assert G(0, D, num, den) == orc.lib().orc_depth_H(D, num, den)
+                # exponential: halve per quarter of the rate
+                want_e = max(1, D >> math.floor(4 * r))
+                # staged: thresholds 1/10, 1/4, 1/2
+                want_s = D if r < Fraction(1, 10) else (D + 1) // 2 if r < Fraction(1, 4) else \
+                    (D + 3) // 4 if r < Fraction(1, 2) else 1
+                got_e, got_s = G(1, D, num, den), G(2, D, num, den)
+                assert got_e == want_e and got_s == want_s
+                assert got_e <= prev[1] and got_s <= prev[2]
+                prev = {1: got_e, 2: got_s}
+            assert G(1, D, 0, den) == D and G(2, D, 0, den) == D
+            assert G(1, D, den, den) == 1 and G(2, D, den, den) == 1
+    assert G(1, 10, 0, 0) == 10 and G(2, 10, 0, 0) == 10      # empty frame keeps D_max
+    assert [G(1, 10, n, 4) for n in range(5)] == [10, 5, 2, 1, 1]
+    assert [G(2, 10, n, 20) for n in (0, 1, 2, 4, 5, 9, 10, 20)] == [10, 10, 5, 5, 3, 3, 1, 1]
+
+
+def test_guide_variants_drive_the_state_machine(orc, c1):
+    """With a partially novel trajectory each guide yields its own depth sequence, and every frame's
+    depth_next is the guide's H of that frame's novelty (the state machine consumes the chosen H)."""
+    cfg, sc = c1
+    c = cfg.center
+    for guide in (1, 2):
+        oc = orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, 10, guide=guide)
+        o = orc.Oracle(sc, oc)
+        for f in range(12):
+            eye = c + np.array([25 * np.cos(0.15 * f), 25 * np.sin(0.15 * f), 2.0 + 0.4 * f])
+            res = o.frame(sg.look_at_rig(eye, c + np.array([0, 0, 3.0]), 0.064), raster=False)
+            st = res.stats
+            if f > 0:
+                assert st.depth_next == orc.lib().orc_depth_H_guide(guide, 10, st.n_new, st.n_visible)
+
+
 # ---------------------------------------------------------------- state machine
 def _oracle(orc, cfg, sc, d_max=None, literal=False):
     oc = orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far,

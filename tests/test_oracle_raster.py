@@ -292,3 +292,43 @@ def test_permutation_invariance(orc, c1):
         setattr(p, k, np.ascontiguousarray(getattr(sc, k)[perm]))
     b = _oracle(orc, cfg, p).frame(rig)
     assert np.array_equal(a.img_l, b.img_l)
+
+
+# ---------------------------------------------------------------- F1 ablations
+def _oracle_abl(orc, cfg, sc, ablate):
+    return orc.Oracle(sc, orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
+                                          ablate=ablate))
+
+
+def test_ablation_aabb_tiles_is_lossless(orc, c1):
+    """AABB tiles (no exact tile test): every candidate tile is kept, so there are more pairs, but a
+    dropped tile never held a pixel with alpha' >= 1/255 (the exact test is lossless), so the
+    pixels are identical; brute force (O1) agrees."""
+    cfg, sc = c1
+    for rig in sg.trajectory(cfg):
+        a = _oracle_abl(orc, cfg, sc, 0).frame(rig)
+        b = _oracle_abl(orc, cfg, sc, 2).frame(rig)
+        assert np.array_equal(a.img_l, b.img_l) and np.array_equal(a.img_r, b.img_r)
+        assert sum(b.stats.n_pairs) >= sum(a.stats.n_pairs)
+    rig = sg.trajectory(cfg)[0]
+    assert sum(_oracle_abl(orc, cfg, sc, 2).frame(rig).stats.n_pairs) > sum(_oracle_abl(orc, cfg, sc, 0).frame(rig).stats.n_pairs)
+
+
+def test_ablation_fixed_extent(orc, c1):
+    """Fixed 3-sigma extent: thr = fl(9 kappa + 2^-6) for every splat; splats with alpha > 0.353
+    (r^2 = 2 ln 255 alpha > 9) lose their contributions beyond 3 sigma ("considering the opacity
+    can scale down the size of the ellipse"), so the image changes, and nothing of significance lies
+    outside the opacity-aware extent of the method, which covers it (lossless)."""
+    cfg, sc = c1
+    rig = sg.trajectory(cfg)[0]
+    o = _oracle_abl(orc, cfg, sc, 1)
+    r1 = o.frame(rig)
+    thr9 = np.float32(np.float32(9.0) * np.float32(1.0009765625)) + np.float32(0.015625)
+    for e in range(2):
+        _, rec = o.splats(e)
+        assert len(rec) and np.all(rec[:, 10] == thr9)
+    r0 = _oracle_abl(orc, cfg, sc, 0).frame(rig)
+    assert not np.array_equal(r0.img_l, r1.img_l)
+    # the method's image equals brute force with no tile cut at all (O1)
+    b = _oracle_abl(orc, cfg, sc, 0).frame(rig, brute=True)
+    assert np.array_equal(r0.img_l, b.img_l)
