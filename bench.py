@@ -133,8 +133,11 @@ def run_gsc(args):
     sc = cfg.scene()
     traj = sg.trajectory(cfg)
     fmt = gp.GSC_FMT_RGBA8
+    free0 = torch.cuda.mem_get_info(dev)[0]
     r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
                     flags=0, pair_capacity=args.pair_capacity).load(sc)
+    torch.cuda.synchronize()
+    mem_bytes = free0 - torch.cuda.mem_get_info(dev)[0]   # the context's device memory (scene, cache, frames)
     out_l, out_r = r.alloc_outputs(fmt)
     stream = torch.cuda.current_stream(dev)
     frames = multi.frame_block(rank, world, len(traj), args.steps)
@@ -270,6 +273,7 @@ def run_gsc(args):
             "stages_note": "CUDA events per stage in a replay of the same frames with GSC_F_SERIAL (no overlap of "
                            "frame f+1's front end with frame f's blend); the timed run overlaps them on two streams",
             "serial_ms_per_frame": round(sum(h["ms_total"] for h in staged) / nf, 4),
+            "device_memory_gb": round(mem_bytes / 1e9, 3),
             # per-frame times of the serial replay ("99% FPS" = 1st percentile of per-frame FPS)
             "frame_ms": {"mean": round(float(np.mean(ft)), 4), "p50": round(float(np.percentile(ft, 50)), 4),
                          "p99": round(float(np.percentile(ft, 99)), 4), "max": round(float(np.max(ft)), 4),
