@@ -61,7 +61,8 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const int px = bx0 + (int)(lane & 7), py = by0 + (int)(lane >> 3);
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
-  const uint2 rg = ranges[tile];
+  // ranges hold (~start, end) (sort.cu, last tile pass); an untouched tile (0, 0) is empty
+  const uint2 rg = make_uint2(~ranges[tile].x, ranges[tile].y);
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   // a lane's liveness floor on power: -inf while it composites, +inf once it has terminated (or lies
   // outside the image), so nothing is live for it any more (one FMNMX instead of a predicate chain)

@@ -31,10 +31,9 @@ void launch_project(const FrameC &, const uint32_t *, const float *, const float
                     uint32_t *, FrameCounters *, int, cudaStream_t);
 int project_tile_size();
 void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, int, const uint32_t *,
-                     uint32_t *, uint32_t *, uint32_t *, int, cudaStream_t);
+                     uint32_t *, uint32_t *, uint32_t *, uint2 *, int, cudaStream_t);
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, int,
                  cudaStream_t);
-void launch_ranges(const uint32_t *, const FrameCounters *, uint2 *, int, cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
                   const float4 *,
                   void *, void *, int, FrameCounters *, bool, cudaStream_t);
@@ -482,7 +481,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   // a5 (depth digits of the (tile, depth) sort)
   launch_onesweep(ctx->dkey_a.p, ctx->dval_a.p, ctx->dkey_b.p, ctx->dval_b.p, true, &ctr->n_splat, 4, 8,
                   &ctr->hist_depth[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[0],
-                  ctx->num_sms, sA);
+                  nullptr, ctx->num_sms, sA);
   mark(sA);
   // the tile keys (eye * T_e + tile) take 2 passes of 7-bit digits when they fit in 14 bits (1080p:
   // 2 T_e = 16320), else of 8-bit digits: 128 bins scatter in longer runs than 256
@@ -491,14 +490,12 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   launch_emit(ei, (uint32_t)ctx->cap_pairs, S.pkey.p, S.pval.p,
               reinterpret_cast<uint32_t *>(S.zero_region.p + ctx->off_emit), ctr, tbits, ctx->num_sms, sA);
   mark(sA);
-  // a6 (tile digits)
+  // a6 (tile digits) + a7 (tile ranges, derived by the last pass)
   launch_onesweep(S.pkey.p, S.pval.p, ctx->pkey_b.p, ctx->pval_b.p, false, &ctr->n_pairs, 2, tbits,
                   &ctr->hist_tile[0][0], ctx->sort_status_a.p, ctx->sort_status_b.p, &ctr->tile_sort[4],
-                  ctx->num_sms, sA);
+                  S.ranges.p, ctx->num_sms, sA);
   mark(sA);
-  // a7
-  launch_ranges(S.pkey.p, ctr, S.ranges.p, ctx->num_sms, sA);
-  mark(sA);
+  mark(sA);   // (a7 has no kernel of its own any more; the stage boundary is kept for the stats layout)
   CU(cudaEventRecord(ctx->ev_a[k], sA));
   // a8 on sB, after the front end and after the caller's earlier work on its stream
   CU(cudaStreamWaitEvent(sB, ctx->ev_a[k], 0));
@@ -759,7 +756,15 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
       return GSC_OK;
     }
-    case GSC_DBG_RANGES: return copy_dev(S.ranges.p, S.ranges.n * 8);
+    case GSC_DBG_RANGES: {   // stored as (~start, end); untouched (empty) tiles as (0, 0)
+      *len = S.ranges.n * 8;
+      if (!host_dst || !cap) return GSC_OK;
+      std::vector<uint2> rg(S.ranges.n);
+      CU(cudaMemcpy(rg.data(), S.ranges.p, S.ranges.n * 8, cudaMemcpyDeviceToHost));
+      for (auto &r : rg) r = r.x ? make_uint2(~r.x, r.y) : make_uint2(0u, 0u);
+      std::memcpy(host_dst, rg.data(), std::min(cap, rg.size() * 8));
+      return GSC_OK;
+    }
     case GSC_DBG_POOL: {
       *len = NK * 13 * 4;
       if (!host_dst || !cap) return GSC_OK;

@@ -1,4 +1,4 @@
-// emit.cu -- SURVEY §8(a) rows a5 (tile-key duplication) and a7 (tile ranges).
+// emit.cu -- SURVEY §8(a) row a5 (tile-key duplication).
 //
 // Duplication happens between the depth digits and the tile digits of the
 // (tile, depth) LSD radix sort (sort.cu): the splats arrive stably sorted by
@@ -14,7 +14,7 @@
 //            are both the biggest and the first in depth order) cost nothing
 //            extra; reads of the list are contiguous runs, writes coalesced.
 //            Fused: the 2 x 256-bin digit histogram of the tile keys.
-//   ranges : [start, end) per (eye, tile) from the tile-sorted keys.
+//   (ranges: derived by the last tile-digit pass of the sort, sort.cu)
 #include "gsc_internal.cuh"
 
 namespace gsc {
@@ -141,44 +141,6 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   }
 }
 
-// 4 keys per thread (one 16-byte load); neighbours across the vector boundary
-// come from the adjacent lane or, at warp edges, one extra cached load.
-__global__ void ranges_kernel(const uint32_t *__restrict__ keys, const FrameCounters *__restrict__ ctr,
-                              uint2 *__restrict__ ranges) {
-  const uint32_t P = ctr->n_pairs;
-  const uint32_t nvec = (P + 3) / 4;
-  const uint32_t lane = lane_id();
-  const uint32_t stride = gridDim.x * blockDim.x;
-  for (uint32_t v0 = blockIdx.x * blockDim.x; v0 < nvec; v0 += stride) {
-    const uint32_t v = v0 + threadIdx.x;
-    const uint32_t p = 4 * v;
-    // the tile key is the low 24 bits (bits 24..31 carry blend.cu's block mask)
-    constexpr uint32_t kM = 0x00FFFFFFu;
-    uint32_t k[4] = {0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu};
-    if (p + 3 < P) {
-      const uint4 q = reinterpret_cast<const uint4 *>(keys)[v];
-      k[0] = q.x & kM; k[1] = q.y & kM; k[2] = q.z & kM; k[3] = q.w & kM;
-    } else {
-      for (int i = 0; i < 4; ++i)
-        if (p + i < P) k[i] = keys[p + i] & kM;
-    }
-    uint32_t prev = __shfl_up_sync(0xFFFFFFFFu, k[3], 1);
-    uint32_t next = __shfl_down_sync(0xFFFFFFFFu, k[0], 1);
-    if (lane == 0) prev = p > 0 && p - 1 < P ? keys[p - 1] & kM : 0xFFFFFFFEu;
-    if (lane == 31) next = p + 4 < P ? keys[p + 4] & kM : 0xFFFFFFFEu;
-    if (p >= P) continue;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const uint32_t q = p + i;
-      if (q >= P) break;
-      const uint32_t before = i == 0 ? prev : k[i - 1];
-      const uint32_t after = (i == 3 || q + 1 >= P) ? (q + 1 >= P ? 0xFFFFFFFEu : next) : k[i + 1];
-      if (q == 0 || before != k[i]) ranges[k[i]].x = q;
-      if (after != k[i]) ranges[k[i]].y = q + 1;
-    }
-  }
-}
-
 static int g_off_grid = 0, g_exp_grid = 0;
 
 void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *vals_out, uint32_t *status,
@@ -192,10 +154,6 @@ void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *v
   }
   pairoff_kernel<<<g_off_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
   expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr, (uint32_t)tbits);
-}
-
-void launch_ranges(const uint32_t *keys, const FrameCounters *ctr, uint2 *ranges, int num_sms, cudaStream_t st) {
-  ranges_kernel<<<num_sms * 4, 256, 0, st>>>(keys, ctr, ranges);
 }
 
 int emit_tile_size() { return kOffTile; }

@@ -32,7 +32,8 @@ struct SplatOut {
   float depth;
 };
 
-__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, int ablate, float alpha,
+template <int kAbl>
+__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float alpha,
                                             const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
   float rho = __fmul_rn(255.0f, alpha);
   if (!(rho > 1.0f)) return false;
@@ -76,7 +77,7 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   o.v = __fadd_rn(__fmul_rn(ec.fy, yz), ec.cy);
   float r2 = __fmul_rn(2.0f, log_s(rho));
   o.r2s = r2;
-  if (ablate & kAblFixedExtent) r2 = 9.0f;   // ablation (GSC_F_ABL_FIXED_EXTENT): fixed 3 sigma
+  if (kAbl & kAblFixedExtent) r2 = 9.0f;   // ablation (GSC_F_ABL_FIXED_EXTENT): fixed 3 sigma
   o.thr = __fadd_rn(__fmul_rn(r2, kKappa), kSlack);
   o.depth = z;
   if (!isfinite(o.A) || !isfinite(o.B) || !isfinite(o.C) || !isfinite(o.u) || !isfinite(o.v) || !isfinite(o.thr))
@@ -269,10 +270,11 @@ constexpr uint32_t kSmallRows = 3;   // boxes of <= 3 tile rows: walked by their
 // upper bound) from the kept-tile list.  A splat whose box has <= kSmallRows rows is walked by its own
 // lane (row by row) into its own area; the rest -- the heavy tail of near, large splats -- are walked
 // cooperatively: their rows laid end to end, 32 rows per step (one per lane), kept keys packed.
+template <bool aabb>
 __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const SplatOut &o, float rx, float ry,
                                                    uint32_t kb, int width, int height, int TW, uint32_t *list,
                                                    uint32_t list_cap, uint32_t *list_top, uint32_t *overflow,
-                                                   bool aabb, uint32_t &list_off) {
+                                                   uint32_t &list_off) {
   const uint32_t lane = lane_id();
   RowSplat r{};
   uint32_t nrows = 0, area = 0;
@@ -375,6 +377,7 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
 // boxes walked as one list) -> kept count and the kept-tile list (row-major
 // keys eye*T_e + ty*TW + tx).  No ordering constraint between warps: each warp
 // bump-allocates its list space.
+template <int kAbl>   // kAbl*: F1 ablations (compile-time, so the method's kernel carries no extra state)
 __global__ void __launch_bounds__(kPThreads)
 project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__restrict__ alpha,
                const float4 *__restrict__ pool, SplatBufs sb, FrameCounters *__restrict__ ctr) {
@@ -403,7 +406,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       q2 = pool[3 * (size_t)g + 2];
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        ok[e] = project_one(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, fc.ablate, al, q0, q1, q2, so[e]);
+        ok[e] = project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, so[e]);
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -419,9 +422,8 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
         ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
       }
       uint32_t loff = 0;
-      const uint32_t n = warp_rows_list(ws, ok[e], o, rx, ry, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
-                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow,
-                                        (fc.ablate & kAblAabbTiles) != 0, loff);
+      const uint32_t n = warp_rows_list<(kAbl & kAblAabbTiles) != 0>(ws, ok[e], o, rx, ry, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
+                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
       if (!valid) continue;
       const uint32_t c = (uint32_t)e * n_live + i;
       uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
@@ -464,11 +466,16 @@ void launch_project(const FrameC &fc, const uint32_t *visible, const float *alph
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, live_kernel, kLThreads, 0);
     g_live_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel, kPThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel<0>, kPThreads, 0);
     g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
   live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_g, status, ctr);
-  project_kernel<<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr);
+  switch (fc.ablate) {
+    case 0: project_kernel<0><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+    case 1: project_kernel<1><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+    case 2: project_kernel<2><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+    default: project_kernel<3><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+  }
 }
 int project_tile_size() { return kLTile; }
 

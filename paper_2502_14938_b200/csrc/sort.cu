@@ -39,10 +39,16 @@ struct SortSmem {
   uint32_t tile;
 };
 
-template <bool kIota>
+// kRanges (the last tile-digit pass): also derive the per-(eye, tile) ranges of the sorted pairs.
+// In SMEM a digit's elements sit in input order, i.e. sorted by the full tile key (low digit sorted by
+// the previous pass), so every run of one key inside the tile's digit segment is visible here; its
+// first and last output positions go to ranges[key] by atomicMax of (~start, end) -- a key split
+// across tiles keeps the smallest start and the largest end.  ranges is zeroed per frame
+// (x = 0 decodes to an empty range).
+template <bool kIota, bool kRanges>
 __global__ void __launch_bounds__(kSThreads, 4)
 onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__restrict__ vals_in,
-                     uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out,
+                     uint32_t *__restrict__ keys_out, uint32_t *__restrict__ vals_out, uint2 *__restrict__ ranges,
                      const uint32_t *__restrict__ d_count, uint32_t shift, uint32_t dmask,
                      const uint32_t *__restrict__ hist,
                      uint32_t *__restrict__ status, uint32_t *__restrict__ status_clear,
@@ -180,6 +186,14 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
       uint32_t o = S.gbase[d] + (i - S.blk_off[d]);
       keys_out[o] = k;
       vals_out[o] = S.vals[i];
+      if (kRanges) {
+        constexpr uint32_t kM = 0x00FFFFFFu;   // tile key (bits 24..31: blend block mask)
+        const uint32_t tk = k & kM;
+        const bool first = i == 0 || (S.keys[i - 1] & kM) != tk;
+        const bool last = i + 1 == nvalid || (S.keys[i + 1] & kM) != tk;
+        if (first) atomicMax(&ranges[tk].x, ~o);
+        if (last) atomicMax(&ranges[tk].y, o + 1);
+      }
     }
   }
 }
@@ -190,19 +204,22 @@ static int g_sort_grid = 0;
 static void sort_setup(int num_sms) {
   if (g_sort_grid) return;
   const int smem = (int)sizeof(SortSmem);
-  cudaFuncSetAttribute(onesweep_pass_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(onesweep_pass_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(onesweep_pass_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(onesweep_pass_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(onesweep_pass_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pass_kernel<false>, kSThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pass_kernel<false, false>, kSThreads, smem);
   g_sort_grid = num_sms * (per_sm > 0 ? per_sm : 1);
 }
 
 // Sort `passes` (even) digits of `bits` bits each (shift 0, bits, 2 bits, ...; bits <= 8) of
 // keys_a[0..*d_count) with payloads vals_a (iota payloads when `iota`).  Ping-pongs a -> b -> a;
-// with an even pass count the result lands back in keys_a / vals_a.
+// with an even pass count the result lands back in keys_a / vals_a.  `ranges` (optional): the last
+// pass also derives the per-tile ranges of the sorted (tile) keys.
 void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint32_t *vals_b, bool iota,
                      const uint32_t *d_count, int passes, int bits, const uint32_t *hist /* [passes][256] */,
-                     uint32_t *status_a, uint32_t *status_b, uint32_t *tile_ctrs, int num_sms, cudaStream_t st) {
+                     uint32_t *status_a, uint32_t *status_b, uint32_t *tile_ctrs, uint2 *ranges, int num_sms,
+                     cudaStream_t st) {
   sort_setup(num_sms);
   const int smem = (int)sizeof(SortSmem);
   const uint32_t dmask = (1u << bits) - 1u;
@@ -213,11 +230,14 @@ void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint3
     uint32_t *stc = odd ? status_b : status_a, *stx = odd ? status_a : status_b;
     const uint32_t shift = (uint32_t)(bits * p);
     if (p == 0 && iota)
-      onesweep_pass_kernel<true><<<g_sort_grid, kSThreads, smem, st>>>(ki, nullptr, ko, vo, d_count, shift, dmask,
-                                                                        hist + 256 * p, stc, stx, tile_ctrs + p);
+      onesweep_pass_kernel<true, false><<<g_sort_grid, kSThreads, smem, st>>>(
+          ki, nullptr, ko, vo, nullptr, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
+    else if (p == passes - 1 && ranges)
+      onesweep_pass_kernel<false, true><<<g_sort_grid, kSThreads, smem, st>>>(
+          ki, vi, ko, vo, ranges, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
     else
-      onesweep_pass_kernel<false><<<g_sort_grid, kSThreads, smem, st>>>(ki, vi, ko, vo, d_count, shift, dmask,
-                                                                         hist + 256 * p, stc, stx, tile_ctrs + p);
+      onesweep_pass_kernel<false, false><<<g_sort_grid, kSThreads, smem, st>>>(
+          ki, vi, ko, vo, nullptr, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
   }
 }
 
