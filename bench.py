@@ -108,8 +108,9 @@ def _stage_bytes(s, N, K, W, H, fmt_bytes):
         "depth_sort": 12 * C + 3 * 16 * C,
         # pairoff 12 B per splat; expand 12 B per pair + 12 B per splat
         "emit": 24 * C + 12 * P,
+        # (the tile ranges are derived inside the last tile pass: no bytes of their own)
         "tile_sort": 2 * 16 * P,
-        "ranges": 4 * P,
+        "ranges": 0.0,
         # pair value + 48-byte record per pair, output images
         "blend": 52 * P + 2 * W * H * fmt_bytes,
     }
@@ -238,7 +239,7 @@ def run_gsc(args):
     kernels = {"blend": ["blend_kernel"], "project": ["live_kernel", "project_kernel"], "cull": ["cull_classify_kernel"],
                "derive": ["derive_mma_kernel"], "depth_sort": ["onesweep_pass_kernel"] * 4,
                "tile_sort": ["onesweep_pass_kernel"] * 2, "emit": ["pairoff_kernel", "expand_kernel"],
-               "ranges": ["ranges_kernel"]}
+               "ranges": []}
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
             tr = json.load(fh)
