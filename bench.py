@@ -246,7 +246,7 @@ def run_gsc(args):
         roof["traffic"] = sum(tr[k]["dram_bytes_per_launch"] for k in kernels[dom])
         roof["traffic_unit"] = "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)"
         roof["traffic_source"] = tr[kernels[dom][0]]["source"]
-    except (OSError, KeyError, ValueError):
+    except (OSError, KeyError, ValueError, IndexError):
         pass
     ft = np.array([h["ms_total"] for h in staged], dtype=np.float64) if staged else np.zeros(1)
     stage_report = {s: {"ms_per_frame": round(ms[s] / nf, 4),
