@@ -33,10 +33,9 @@ struct SplatOut {
 };
 
 template <int kAbl>
-__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float alpha,
+__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float r2s,
                                             const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
-  float rho = __fmul_rn(255.0f, alpha);
-  if (!(rho > 1.0f)) return false;
+  // (the live test 255 alpha > 1 was made by live_kernel; r2s = 2 ln(255 alpha) is eye-independent)
   float t0 = __fsub_rn(p0.x, ec.p[0]), t1 = __fsub_rn(p0.y, ec.p[1]), t2 = __fsub_rn(p0.z, ec.p[2]);
   float x = dot3(t0, t1, t2, ec.r0), y = dot3(t0, t1, t2, ec.r1), z = dot3(t0, t1, t2, ec.r2);
   if (!(z > ec.near_plane) || z > ec.far_plane) return false;
@@ -75,8 +74,8 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   o.C = __fdiv_rn(a, det);
   o.u = __fadd_rn(__fmul_rn(ec.fx, xz), ec.cx);
   o.v = __fadd_rn(__fmul_rn(ec.fy, yz), ec.cy);
-  float r2 = __fmul_rn(2.0f, log_s(rho));
-  o.r2s = r2;
+  float r2 = r2s;
+  o.r2s = r2s;
   if (kAbl & kAblFixedExtent) r2 = 9.0f;   // ablation (GSC_F_ABL_FIXED_EXTENT): fixed 3 sigma
   o.thr = __fadd_rn(__fmul_rn(r2, kKappa), kSlack);
   o.depth = z;
@@ -404,9 +403,10 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       const float4 q0 = pool[3 * (size_t)g];
       const float4 q1 = pool[3 * (size_t)g + 1];
       q2 = pool[3 * (size_t)g + 2];
+      const float r2s = __fmul_rn(2.0f, log_s(__fmul_rn(255.0f, al)));   // r^2 = 2 ln(alpha/eps)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        ok[e] = project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, al, q0, q1, q2, so[e]);
+        ok[e] = project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, so[e]);
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
