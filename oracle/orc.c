@@ -366,12 +366,13 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
   float t[3] = {mu[0] - ec->p[0], mu[1] - ec->p[1], mu[2] - ec->p[2]};
   float x = dot3(t, ec->r0), y = dot3(t, ec->r1), z = dot3(t, ec->r2);
   if (!(z > ec->near_plane) || z > ec->far_plane) return 0; /* S:349 */
-  float xz = x / z, yz = y / z;
+  /* N8: one reciprocal of z (and of det below), rounded once, multiplied in */
+  float iz = 1.0f / z, iz2 = iz * iz;
+  float xz = x * iz, yz = y * iz;
   float xc = fminf(fmaxf(xz, -ec->limx), ec->limx) * z;
   float yc = fminf(fmaxf(yz, -ec->limy), ec->limy) * z;
-  float zz = z * z;
-  float J00 = ec->fx / z, J02 = -(ec->fx * xc) / zz;
-  float J11 = ec->fy / z, J12 = -(ec->fy * yc) / zz;
+  float J00 = ec->fx * iz, J02 = -(ec->fx * xc) * iz2;
+  float J11 = ec->fy * iz, J12 = -(ec->fy * yc) * iz2;
   float T[2][3];
   for (int k = 0; k < 3; ++k) {
     T[0][k] = (J00 * ec->r0[k]) + (J02 * ec->r2[k]);
@@ -388,9 +389,10 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
   c = c + 0.3f;
   float det = (a * c) - (b * b);
   if (!(det > 0.0f)) return 0;
-  o->A = c / det;
-  o->B = (-b) / det;
-  o->C = a / det;
+  float idet = 1.0f / det;
+  o->A = c * idet;
+  o->B = (-b) * idet;
+  o->C = a * idet;
   o->u = (ec->fx * xz) + ec->cx;
   o->v = (ec->fy * yz) + ec->cy;
   float r2 = 2.0f * orc_log_s(rho);                         /* r^2 = 2 ln(alpha/eps) */

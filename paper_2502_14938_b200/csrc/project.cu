@@ -39,12 +39,13 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   float t0 = __fsub_rn(p0.x, ec.p[0]), t1 = __fsub_rn(p0.y, ec.p[1]), t2 = __fsub_rn(p0.z, ec.p[2]);
   float x = dot3(t0, t1, t2, ec.r0), y = dot3(t0, t1, t2, ec.r1), z = dot3(t0, t1, t2, ec.r2);
   if (!(z > ec.near_plane) || z > ec.far_plane) return false;
-  float xz = __fdiv_rn(x, z), yz = __fdiv_rn(y, z);
+  // N8: one reciprocal of z (and of det below), rounded once, multiplied in
+  const float iz = __fdiv_rn(1.0f, z), iz2 = __fmul_rn(iz, iz);
+  float xz = __fmul_rn(x, iz), yz = __fmul_rn(y, iz);
   float xc = __fmul_rn(fminf(fmaxf(xz, -ec.limx), ec.limx), z);
   float yc = __fmul_rn(fminf(fmaxf(yz, -ec.limy), ec.limy), z);
-  float zz = __fmul_rn(z, z);
-  float J00 = __fdiv_rn(ec.fx, z), J02 = __fdiv_rn(-__fmul_rn(ec.fx, xc), zz);
-  float J11 = __fdiv_rn(ec.fy, z), J12 = __fdiv_rn(-__fmul_rn(ec.fy, yc), zz);
+  float J00 = __fmul_rn(ec.fx, iz), J02 = __fmul_rn(-__fmul_rn(ec.fx, xc), iz2);
+  float J11 = __fmul_rn(ec.fy, iz), J12 = __fmul_rn(-__fmul_rn(ec.fy, yc), iz2);
   float T[2][3];
 #pragma unroll
   for (int k = 0; k < 3; ++k) {
@@ -69,9 +70,10 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   if (!(det > 0.0f)) return false;
   o.sxx = a;
   o.syy = c;
-  o.A = __fdiv_rn(c, det);
-  o.B = __fdiv_rn(-b, det);
-  o.C = __fdiv_rn(a, det);
+  const float idet = __fdiv_rn(1.0f, det);
+  o.A = __fmul_rn(c, idet);
+  o.B = __fmul_rn(-b, idet);
+  o.C = __fmul_rn(a, idet);
   o.u = __fadd_rn(__fmul_rn(ec.fx, xz), ec.cx);
   o.v = __fadd_rn(__fmul_rn(ec.fy, yz), ec.cy);
   float r2 = r2s;
