@@ -263,3 +263,34 @@ def test_host_async_matches_device_render(orc, c1):
         r2.wait_frame(q)
     for (hl, hr), (wl, wr) in zip(bufs, want):
         assert torch.equal(hl, wl) and torch.equal(hr, wr)
+
+
+def test_elastic_session_real_time(orc, c1):
+    """F2 in real time on the GPU: two workers with private pipelines (C1 scene) fed by the shared
+    queue at 200 Hz for 2 s; frames render end to end, displayed timestamps are monotone, no stale
+    pose is rendered."""
+    import torch
+    import paper_2502_14938_b200 as gp
+    from paper_2502_14938_b200 import elastic as el
+    cfg, sc = c1
+    c = cfg.center
+
+    def make_worker(w):
+        r = renderer(cfg).load(sc)
+        hl = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
+        hr = torch.empty((cfg.height, cfg.width, 4), dtype=torch.uint8).pin_memory()
+
+        def render(rig):
+            r.render_host(rig, hl, hr, gp.GSC_FMT_RGBA8)
+            return {}
+        return render
+
+    poses = [sg.look_at_rig(c + np.array([25 * np.cos(0.01 * k), 25 * np.sin(0.01 * k), 3.0]), c, 0.064)
+             for k in range(400)]
+    scfg = el.SessionConfig(w_init=2, w_max=2, control=False, sample_interval=1 / 200.0, timeout=0.1)
+    rep = el.run_session(poses, scfg, clock="real", make_worker=make_worker, duration=2.0)
+    ts = rep.displayed_ts
+    assert rep.n_displayed > 50
+    assert all(a <= b for a, b in zip(ts, ts[1:]))
+    assert all(r.t_start - r.timestamp <= scfg.timeout + 0.01 for r in rep.records)
+    assert {r.worker for r in rep.records} == {0, 1}
