@@ -73,6 +73,9 @@ typedef struct gsc_ctx gsc_ctx;
                                         of the opacity-aware 2 ln(255 alpha); the blend is unchanged */
 #define GSC_F_ABL_AABB_TILES 0x100u  /* ablation (F1): keep every tile of the candidate box (no exact tile test,
                                         P:256) -- more pairs, same pixels */
+#define GSC_F_MONO 0x200u           /* render the left eye only (the right image is left untouched); with a
+                                        rig whose eyes coincide this is a monocular pipeline -- two such
+                                        contexts, one per eye, are the no-de-redundancy ablation (F1) */
 #define GSC_F_SERIAL 0x10u       /* do not overlap frame f+1's front end (cull .. ranges) with frame f's
                                     blend: per-stage times then add up to the frame time */
 

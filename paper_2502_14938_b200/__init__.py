@@ -11,13 +11,13 @@ import math
 
 from . import _abi
 from ._abi import (GSC_F_ABL_AABB_TILES, GSC_F_ABL_FIXED_EXTENT, GSC_F_COUNT_EVALS, GSC_F_DEPTH_LITERAL,
-                   GSC_F_DERIVE_CUDA_CORES, GSC_F_GUIDE_EXP,
+                   GSC_F_DERIVE_CUDA_CORES, GSC_F_GUIDE_EXP, GSC_F_MONO,
                    GSC_F_GUIDE_STAGED, GSC_F_SERIAL, GSC_F_STAGE_TIMING,
                    GSC_FMT_RGB_F32_PLANAR, GSC_FMT_RGBA8, GscError, gsc_frame_stats)
 
 __all__ = ["Renderer", "GscError", "GSC_F_DEPTH_LITERAL", "GSC_F_STAGE_TIMING", "GSC_F_DERIVE_CUDA_CORES",
            "GSC_F_COUNT_EVALS", "GSC_F_SERIAL", "GSC_F_GUIDE_EXP", "GSC_F_GUIDE_STAGED", "GSC_F_ABL_FIXED_EXTENT",
-           "GSC_F_ABL_AABB_TILES", "GSC_FMT_RGB_F32_PLANAR",
+           "GSC_F_ABL_AABB_TILES", "GSC_F_MONO", "PerEyeRenderer", "GSC_FMT_RGB_F32_PLANAR",
            "GSC_FMT_RGBA8", "build"]
 
 
@@ -176,3 +176,33 @@ class Renderer:
         self._chk(_abi.lib().gsc_selftest_elementary(self.h, code, C.c_void_p(x.data_ptr()),
                                                      C.c_void_p(out.data_ptr()), x.numel()))
         return out
+
+
+class PerEyeRenderer:
+    """The no-de-redundancy ablation (the baseline of P:216-225): one monocular
+    GS-Cache pipeline per eye -- its own cull, cache, derivation (through that eye's own viewpoint),
+    projection, sort and blend -- instead of one unified cull + derivation shared by both eyes.  Each
+    eye's context renders a rig whose two eyes coincide with that eye (GSC_F_MONO: left image only)."""
+
+    def __init__(self, device: int, width: int, height: int, fov_y_deg: float = 70.0, near: float = 0.05,
+                 far: float = 5000.0, d_max: int = 10, bg=(0.0, 0.0, 0.0), flags: int = 0, pair_capacity: int = 0):
+        self.eyes = [Renderer(device, width, height, fov_y_deg, near, far, d_max, bg=bg, flags=flags | GSC_F_MONO,
+                              pair_capacity=pair_capacity) for _ in range(2)]
+
+    def load(self, scene):
+        for r in self.eyes:
+            r.load(scene)
+        return self
+
+    @staticmethod
+    def _mono(rig, e):
+        import dataclasses
+        p, q = (rig.lp, rig.lq) if e == 0 else (rig.rp, rig.rq)
+        return dataclasses.replace(rig, lp=p, lq=q, rp=p, rq=q)
+
+    def render(self, rig, fmt: int = GSC_FMT_RGB_F32_PLANAR):
+        """(left, right, [stats_left_pipeline, stats_right_pipeline])"""
+        ol, _, sl = self.eyes[0].render(self._mono(rig, 0), fmt)
+        orr, _, sr = self.eyes[1].render(self._mono(rig, 1), fmt)
+        return ol, orr, [sl, sr]
+

@@ -157,10 +157,11 @@ void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_ke
                   const float4 *spA,
                   const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, FrameCounters *ctr,
                   bool count, cudaStream_t st) {
+  const int grid = (fc.ablate & kAblMono) ? fc.Te : 2 * fc.Te;   // GSC_F_MONO: left eye tiles only
   if (count)
-    blend_kernel<true><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<true><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
   else
-    blend_kernel<false><<<2 * fc.Te, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<false><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
 }
 
 // elementary-function self test (parity sweeps through the C ABI)

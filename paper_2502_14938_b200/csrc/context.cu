@@ -455,7 +455,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   if (ctx->b_pending[k]) CU(cudaStreamWaitEvent(sA, ctx->ev_b[k], 0));   // blend f-2 done with set k
   FrameCounters *ctr = S.ctr();
   ctx->fc.ablate = ((ctx->cfg.flags & GSC_F_ABL_FIXED_EXTENT) ? kAblFixedExtent : 0) |
-                   ((ctx->cfg.flags & GSC_F_ABL_AABB_TILES) ? kAblAabbTiles : 0);
+                   ((ctx->cfg.flags & GSC_F_ABL_AABB_TILES) ? kAblAabbTiles : 0) |
+                   ((ctx->cfg.flags & GSC_F_MONO) ? kAblMono : 0);
   const FrameC &fc = ctx->fc;
   mark(sA);
   CU(cudaMemsetAsync(S.zero_region.p, 0, ctx->zero_bytes, sA));
@@ -699,7 +700,7 @@ gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
   if (!ctx) return GSC_EINVAL;
   const unsigned known =
       GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL |
-      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES;
+      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES | GSC_F_MONO;
   if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
   if ((flags & GSC_F_GUIDE_EXP) && (flags & GSC_F_GUIDE_STAGED)) return fail(ctx, GSC_EINVAL, "two guiding functions");
   CU(cudaSetDevice(ctx->device));

@@ -35,6 +35,7 @@ struct FrameC {
 };
 constexpr int kAblFixedExtent = 1;
 constexpr int kAblAabbTiles = 2;
+constexpr int kAblMono = 4;       // GSC_F_MONO: left eye only (per-eye pipelines of the no-de-redundancy ablation)
 
 // ---- device-resident counters, zeroed at every frame start ----
 struct FrameCounters {

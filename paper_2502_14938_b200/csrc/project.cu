@@ -408,7 +408,8 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       const float r2s = __fmul_rn(2.0f, log_s(__fmul_rn(255.0f, al)));   // r^2 = 2 ln(alpha/eps)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
-        ok[e] = project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, so[e]);
+        ok[e] = (e == 1 && (kAbl & kAblMono)) ? false   // GSC_F_MONO: the right eye is not rendered
+                : project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, so[e]);
     }
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -473,10 +474,12 @@ void launch_project(const FrameC &fc, const uint32_t *visible, const float *alph
   }
   live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_g, status, ctr);
   switch (fc.ablate) {
-    case 0: project_kernel<0><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
-    case 1: project_kernel<1><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
-    case 2: project_kernel<2><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
-    default: project_kernel<3><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+#define GSC_PROJ_CASE(k) \
+  case k: project_kernel<k><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+    GSC_PROJ_CASE(0) GSC_PROJ_CASE(1) GSC_PROJ_CASE(2) GSC_PROJ_CASE(3)
+    GSC_PROJ_CASE(4) GSC_PROJ_CASE(5) GSC_PROJ_CASE(6) GSC_PROJ_CASE(7)
+#undef GSC_PROJ_CASE
+    default: break;
   }
 }
 int project_tile_size() { return kLTile; }

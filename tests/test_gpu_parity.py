@@ -294,3 +294,23 @@ def test_elastic_session_real_time(orc, c1):
     assert all(a <= b for a, b in zip(ts, ts[1:]))
     assert all(r.t_start - r.timestamp <= scfg.timeout + 0.01 for r in rep.records)
     assert {r.worker for r in rep.records} == {0, 1}
+
+
+def test_c1_no_dered_per_eye_pipelines(orc, c1):
+    """No-de-redundancy ablation (F1): one monocular pipeline per eye (PerEyeRenderer, GSC_F_MONO)
+    equals, eye by eye, an oracle state machine driven by that eye alone (a rig whose eyes coincide):
+    visible / hit / miss sets every frame and the eye's image bit for bit, over a moving trajectory."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    per = gp.PerEyeRenderer(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, 4).load(sc)
+    oracles = [orc.Oracle(sc, oracle_config(orc, cfg, d_max=4)) for _ in range(2)]
+    c = cfg.center
+    for f in range(12):
+        eye = c + np.array([25 * np.cos(0.12 * f), 25 * np.sin(0.12 * f), 2.0 + 0.5 * f])
+        rig = sg.look_at_rig(eye, c + np.array([0, 0, 3.0]), 0.064)
+        il, ir, stats = per.render(rig)
+        for e, img in enumerate((il, ir)):
+            res = oracles[e].frame(gp.PerEyeRenderer._mono(rig, e))
+            compare_sets(oracles[e], per.eyes[e], stats[e])
+            d = float(np.abs(img.cpu().numpy() - res.img_l).max())
+            assert d == 0.0

@@ -68,6 +68,7 @@ def run(config="C3", frames=150):
         "abl_fixed_extent": (cfg.d_max, gp.GSC_F_ABL_FIXED_EXTENT),
         "abl_aabb_tiles": (cfg.d_max, gp.GSC_F_ABL_AABB_TILES),
         "no_reuse": (1, 0),
+        "no_dered": (cfg.d_max, "per_eye"),      # one monocular pipeline per eye (F1)
     }
     # reference images: uncached (D_max = 1), opacity-aware extent, exact tiles
     ref_r = gp.Renderer(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, 1).load(sc)
@@ -79,22 +80,26 @@ def run(config="C3", frames=150):
     out = {"config": config, "frames": len(traj), "reference": "uncached (D_max = 1) render of every frame",
            "variants": {}}
     for name, (dmax, flags) in variants.items():
+        per_eye = flags == "per_eye"
+        flags = 0 if per_eye else flags
         # (AABB tiles need more pair capacity than the default 4 N K)
         cap = max(3 << 24, 12 * sc.n * 10) if flags & gp.GSC_F_ABL_AABB_TILES else 0
-        r = gp.Renderer(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, dmax,
-                        flags=flags | gp.GSC_F_STAGE_TIMING | gp.GSC_F_SERIAL, pair_capacity=cap).load(sc)
+        R = gp.PerEyeRenderer if per_eye else gp.Renderer
+        r = R(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, dmax,
+              flags=flags | gp.GSC_F_STAGE_TIMING | gp.GSC_F_SERIAL, pair_capacity=cap).load(sc)
         ps, ss, ms_, misses, pairs = [], [], [], [], []
         for (rig, (rl, rr)) in zip(traj, refs):
             gl, gr, st = r.render(rig)
             p = min(psnr(gl, rl), psnr(gr, rr))
             ps.append(p if np.isfinite(p) else 99.0)
             ss.append(0.5 * (ssim(gl, rl) + ssim(gr, rr)))
-            misses.append(st["n_misses"] / max(1, st["n_visible"]))
-            pairs.append(st["n_pairs"])
-            ms_.append(st["ms_total"])
+            sts = st if isinstance(st, list) else [st]
+            misses.append(sum(x["n_misses"] for x in sts) / max(1, sum(x["n_visible"] for x in sts)))
+            pairs.append(sum(x["n_pairs"] for x in sts))
+            ms_.append(sum(x["ms_total"] for x in sts))
         ms_ = np.array(ms_)
         out["variants"][name] = {
-            "d_max": dmax, "flags": flags,
+            "d_max": dmax, "flags": "per-eye pipelines" if per_eye else flags,
             "psnr_mean_db": round(float(np.mean(ps)), 3), "psnr_min_db": round(float(np.min(ps)), 3),
             "ssim_mean": round(float(np.mean(ss)), 6), "ssim_min": round(float(np.min(ss)), 6),
             "update_rate_mean": round(float(np.mean(misses)), 4), "pairs_mean": round(float(np.mean(pairs))),
