@@ -240,6 +240,22 @@ def test_c4_full_size_bench_config(orc, c4):
             assert d == 0.0
 
 
+def test_c5_full_size_frames(orc):
+    """configs[4] (5M anchors, 2K binocular, the scaling workload) at full size: frame 0 (cold cache,
+    every visible anchor derived) and frame 10 (after 9 cached frames) fully bit-exact -- sets, pool,
+    splat records, sorted keys, pixels -- with the hit/miss sets of the frames between."""
+    cfg = sg.config("C5")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(11):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in (0, 10))
+        assert not st["overflow"]
+        if f in (0, 10):
+            assert d == 0.0
+
+
 def test_host_async_matches_device_render(orc, c1):
     """The asynchronous end-to-end API (host pose in, images into pinned host memory, frame f's copy
     overlapping frame f+1) returns the same images as device rendering, frame by frame, through a
