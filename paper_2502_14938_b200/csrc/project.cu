@@ -379,7 +379,7 @@ __device__ __forceinline__ uint32_t warp_rows_list(WarpRows &ws, bool has, const
 // keys eye*T_e + ty*TW + tx).  No ordering constraint between warps: each warp
 // bump-allocates its list space.
 template <int kAbl>   // kAbl*: F1 ablations (compile-time, so the method's kernel carries no extra state)
-__global__ void __launch_bounds__(kPThreads)
+__global__ void __launch_bounds__(kPThreads, 4)   // 64 registers: 4 CTAs / SM (measured better than 80 / 3)
 project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__restrict__ alpha,
                const float4 *__restrict__ pool, SplatBufs sb, FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_hist[4][256];
@@ -391,11 +391,15 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
   const uint32_t n_live = ctr->n_splat / 2;
   const uint32_t nw = (gridDim.x * kPThreads) >> 5;
   uint32_t pairs_local = 0;
-  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 32 + warp * 32; base < n_live; base += nw * 32) {
-    const uint32_t i = base + lane;
+  // lane = (item, eye): 16 live Gaussians per warp step, lanes 2k / 2k+1 take Gaussian k's left / right
+  // eye (half the per-thread state of a lane doing both eyes: more warps in flight)
+  const uint32_t e = lane & 1u;
+  const EyeC &ec = e ? fc.eye[1] : fc.eye[0];
+  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 16 + warp * 16; base < n_live; base += nw * 16) {
+    const uint32_t i = base + (lane >> 1);
     const bool valid = i < n_live;
-    SplatOut so[2];
-    bool ok[2] = {false, false};
+    SplatOut o;
+    bool ok = false;
     uint32_t g = 0;
     float al = 0.0f;
     float4 q2 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -406,49 +410,44 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       const float4 q1 = pool[3 * (size_t)g + 1];
       q2 = pool[3 * (size_t)g + 2];
       const float r2s = __fmul_rn(2.0f, log_s(__fmul_rn(255.0f, al)));   // r^2 = 2 ln(alpha/eps)
-#pragma unroll
-      for (int e = 0; e < 2; ++e)
-        ok[e] = (e == 1 && (kAbl & kAblMono)) ? false   // GSC_F_MONO: the right eye is not rendered
-                : project_one<kAbl>(fc.eye[e], fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, so[e]);
+      ok = (e == 1 && (kAbl & kAblMono)) ? false   // GSC_F_MONO: the right eye is not rendered
+           : project_one<kAbl>(ec, fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, o);
     }
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const SplatOut &o = so[e];
-      // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure; (rx, ry) =
-      // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel outside them
-      // has power < pmin, so the blend may skip it without changing a decision
-      float pmin = 0.0f, rx = 0.0f, ry = 0.0f;
-      if (ok[e]) {
-        pmin = __fsub_rn(__fmul_rn(-0.5f, o.r2s), 0.0078125f);
-        const float qmax = __fmul_rn(-2.0f, pmin);
-        rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
-        ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
-      }
-      uint32_t loff = 0;
-      const uint32_t n = warp_rows_list<(kAbl & kAblAabbTiles) != 0>(ws, ok[e], o, rx, ry, e ? (uint32_t)fc.Te : 0u, fc.width, fc.height,
-                                        fc.TW, sb.list, sb.list_cap, &ctr->list_top, &ctr->overflow, loff);
-      if (!valid) continue;
-      const uint32_t c = (uint32_t)e * n_live + i;
-      uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
-      if (ok[e]) {
-        // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
-        dk = __float_as_uint(o.depth);
-        sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
-        sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
-        sb.box[c] = make_uint2(o.box_x, o.box_y | ((uint32_t)e << 31));
-        sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
-        sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
-      } else {
-        sb.box[c] = make_uint2(0x0000FFFFu, (uint32_t)e << 31);   // tx0 = 65535 > tx1 = 0: empty
-      }
-      sb.depth[c] = dk;
-      sb.gslot[c] = g;
-      sb.count[c] = n;
-      sb.list_off[c] = loff;
-      pairs_local += n;
-#pragma unroll
-      for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
+    // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure; (rx, ry) =
+    // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel outside them
+    // has power < pmin, so the blend may skip it without changing a decision
+    float pmin = 0.0f, rx = 0.0f, ry = 0.0f;
+    if (ok) {
+      pmin = __fsub_rn(__fmul_rn(-0.5f, o.r2s), 0.0078125f);
+      const float qmax = __fmul_rn(-2.0f, pmin);
+      rx = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.sxx)), 1.001f), 0.01f);
+      ry = __fadd_rn(__fmul_rn(__fsqrt_rn(__fmul_rn(qmax, o.syy)), 1.001f), 0.01f);
     }
+    uint32_t loff = 0;
+    const uint32_t n = warp_rows_list<(kAbl & kAblAabbTiles) != 0>(ws, ok, o, rx, ry, e ? (uint32_t)fc.Te : 0u,
+                                                                  fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
+                                                                  &ctr->list_top, &ctr->overflow, loff);
+    if (!valid) continue;
+    const uint32_t c = e * n_live + i;
+    uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
+    if (ok) {
+      // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
+      dk = __float_as_uint(o.depth);
+      sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
+      sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
+      sb.box[c] = make_uint2(o.box_x, o.box_y | (e << 31));
+      sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
+      sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
+    } else {
+      sb.box[c] = make_uint2(0x0000FFFFu, e << 31);   // tx0 = 65535 > tx1 = 0: empty
+    }
+    sb.depth[c] = dk;
+    sb.gslot[c] = g;
+    sb.count[c] = n;
+    sb.list_off[c] = loff;
+    pairs_local += n;
+#pragma unroll
+    for (int d = 0; d < 4; ++d) atomicAdd(&s_hist[d][(dk >> (8 * d)) & 0xFFu], 1u);
   }
   for (int o = 16; o > 0; o >>= 1) pairs_local += __shfl_xor_sync(0xFFFFFFFFu, pairs_local, o);
   if (lane == 0 && pairs_local) atomicAdd(&ctr->n_pairs_raw, pairs_local);
