@@ -8,7 +8,9 @@
 // (255 alpha > 1; Gaussian g = X_f[v]*K + j) into live_g, in s order (hence
 // ascending g), with a CTA-level decoupled look-back over 4096-slot tiles: it
 // only reads 4 bytes per slot, so its look-back chain is short.
-// project_kernel then projects live item i for both eyes with every lane busy
+// project_kernel then projects live item i for eye e in lane (i, e) -- every
+// lane busy -- walks the kept tiles of the warp's 32 splats (exact row-form
+// tile test, N7) into the kept-tile list with each pair's blend-block mask,
 // and writes splat c = e * n_live + i: per eye, c ascends with g -- the order
 // that makes the later stable sorts break depth ties by g like the oracle.
 // Live splats that project nowhere keep an entry with an empty box (0 tiles).
