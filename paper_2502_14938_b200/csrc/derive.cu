@@ -192,7 +192,7 @@ __global__ void __launch_bounds__(kDThreads) derive_kernel(DeriveArgs p) {
 }
 
 // ------------------------------------------------------------------ tensor-core kernel (tcgen05, kind::i8)
-constexpr int kMThreads = 256;
+constexpr int kMThreads = 512;
 constexpr int kMA = 128;                 // anchors per tile = UMMA M
 constexpr int kTmemCols = 512;
 // TMEM column map (32-bit cells): layer-2 accumulators D2[h][l], then D1
