@@ -7,7 +7,7 @@
 // order ("key-value pairs").
 //
 //   pairoff: exclusive scan of the kept-tile counts in depth order
-//            (CTA tiles of 4096, CTA-wide decoupled look-back) -> pair_off[p], P
+//            (CTA tiles of 4096, reduce-then-scan) -> pair_off[p], P
 //   expand : load-balanced expansion -- each warp owns 256 consecutive OUTPUT
 //            positions q and finds the owning splat by a 32-ary cooperative
 //            search of pair_off, so the heavy-tailed splat sizes (near splats
@@ -25,25 +25,58 @@ constexpr int kOffTile = kXThreads * kOffItems;   // 4096 sorted positions per C
 constexpr int kExpItems = 8;
 constexpr int kExpChunk = 32 * kExpItems;  // output positions per warp chunk
 
+// Exclusive scan of the kept counts in depth order as reduce-then-scan (no look-back: a single-pass
+// scan spends most of its time waiting for predecessor tiles at this size).
+//   pairoff_reduce: agg[tile] = sum of the tile's 4096 counts (tiles independent)
+//   pairoff_scan:   prefix(tile) = sum of agg[< tile] (CTA-parallel, L2-resident), then the tile's
+//                   local scan -> pair_off; the last tile also sets n_pairs / overflow.
+__device__ __forceinline__ void pairoff_counts(const EmitIn &in, uint32_t C, uint32_t tile, uint32_t (&cnt)[kOffItems]) {
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;   // warp w: positions [w*512, +512)
+#pragma unroll
+  for (int i = 0; i < kOffItems; ++i) {
+    const uint32_t p = p0 + 32 * i;
+    cnt[i] = p < C ? in.count[in.sorted[p]] : 0u;
+  }
+}
+
 __global__ void __launch_bounds__(kXThreads)
-pairoff_kernel(EmitIn in, uint32_t cap, uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_cnt[kXThreads / 32], s_red[kXThreads / 32 + 1], s_tile;
+pairoff_reduce_kernel(EmitIn in, uint32_t *__restrict__ agg, const FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_w[kXThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t C = ctr->n_splat;
   const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_pairoff, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    // warp w owns positions [tile*4096 + w*512, +512), 16 rounds of 32
-    const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;
-    uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t cnt[kOffItems], sum = 0;
+    pairoff_counts(in, C, tile, cnt);
 #pragma unroll
-    for (int i = 0; i < kOffItems; ++i) {
-      const uint32_t p = p0 + 32 * i;
-      cnt[i] = p < C ? in.count[in.sorted[p]] : 0u;
+    for (int i = 0; i < kOffItems; ++i) sum += cnt[i];
+    sum = __reduce_add_sync(0xFFFFFFFFu, sum);
+    if (lane == 0) s_w[warp] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kXThreads / 32; ++w) t += s_w[w];
+      agg[tile] = t;
     }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kXThreads)
+pairoff_scan_kernel(EmitIn in, uint32_t cap, const uint32_t *__restrict__ agg, FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_cnt[kXThreads / 32], s_pre[kXThreads / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
+  const uint32_t C = ctr->n_splat;
+  const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
+    pairoff_counts(in, C, tile, cnt);
+    // prefix of the earlier tiles
+    uint32_t pre = 0;
+    for (uint32_t j = threadIdx.x; j < tile; j += kXThreads) pre += agg[j];
+    pre = __reduce_add_sync(0xFFFFFFFFu, pre);
 #pragma unroll
     for (int i = 0; i < kOffItems; ++i) {
       uint32_t inc = cnt[i];
@@ -55,32 +88,29 @@ pairoff_kernel(EmitIn in, uint32_t cap, uint32_t *__restrict__ status, FrameCoun
       excl[i] = run + inc - cnt[i];
       run += __shfl_sync(0xFFFFFFFFu, inc, 31);
     }
-    if (lane == 0) s_cnt[warp] = run;
+    if (lane == 0) { s_cnt[warp] = run; s_pre[warp] = pre; }
     __syncthreads();
-    uint32_t wex = 0, agg = 0;
+    uint32_t wex = 0, tot = 0;
+    pre = 0;
 #pragma unroll
     for (int w = 0; w < kXThreads / 32; ++w) {
       const uint32_t c = s_cnt[w];
       wex += (uint32_t)w < warp ? c : 0u;
-      agg += c;
+      tot += c;
+      pre += s_pre[w];
     }
-    if (threadIdx.x == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-    uint32_t pre = 0;
-    if (tile > 0) {
-      pre = block_lookback_u32<kXThreads>(status, tile, s_red);
-      if (threadIdx.x == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-    }
+    const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;
 #pragma unroll
     for (int i = 0; i < kOffItems; ++i) {
       const uint32_t p = p0 + 32 * i;
       if (p < C) in.pair_off[p] = pre + wex + excl[i];
     }
     if (threadIdx.x == 0 && tile == ntiles - 1) {
-      const uint32_t tot = pre + agg;
-      ctr->n_pairs = tot < cap ? tot : cap;
-      if (tot > cap) ctr->overflow = 1u;
+      const uint32_t all = pre + tot;
+      ctr->n_pairs = all < cap ? all : cap;
+      if (all > cap) ctr->overflow = 1u;
     }
-    __syncthreads();   // s_cnt / s_tile reuse
+    __syncthreads();   // s_cnt / s_pre reuse
   }
 }
 
@@ -141,18 +171,21 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   }
 }
 
-static int g_off_grid = 0, g_exp_grid = 0;
+static int g_red_grid = 0, g_scan_grid = 0, g_exp_grid = 0;
 
 void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *vals_out, uint32_t *status,
                  FrameCounters *ctr, int tbits, int num_sms, cudaStream_t st) {
-  if (!g_off_grid) {
+  if (!g_scan_grid) {
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_kernel, kXThreads, 0);
-    g_off_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_reduce_kernel, kXThreads, 0);
+    g_red_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_scan_kernel, kXThreads, 0);
+    g_scan_grid = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_kernel, kXThreads, 0);
     g_exp_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
-  pairoff_kernel<<<g_off_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
+  pairoff_reduce_kernel<<<g_red_grid, kXThreads, 0, st>>>(in, status, ctr);
+  pairoff_scan_kernel<<<g_scan_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
   expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr, (uint32_t)tbits);
 }
 
