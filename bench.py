@@ -236,7 +236,7 @@ def run_gsc(args):
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
                 "note": f"algorithmic bytes/frame {algo[dom] / nf:.4g}; peak {peaks['src']}"}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    kernels = {"blend": ["blend_kernel"], "project": ["live_kernel", "project_kernel"], "cull": ["cull_classify_kernel"],
+    kernels = {"blend": ["blend_kernel"], "project": ["live_kernel", "project_kernel"], "cull": ["cull_classify_kernel", "cull_compact_kernel"],
                "derive": ["derive_mma_kernel"], "depth_sort": ["onesweep_pass_kernel"] * 4,
                "tile_sort": ["onesweep_pass_kernel"] * 2, "emit": ["pairoff_kernel", "expand_kernel"],
                "ranges": []}

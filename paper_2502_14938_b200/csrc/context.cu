@@ -19,8 +19,8 @@
 namespace gsc {
 // launchers (kernels in the other translation units)
 void launch_cull(const FrameC &, int, const float4 *, const uint8_t *, int32_t *, const uint32_t *, uint32_t *,
-                 uint32_t *, uint32_t *, unsigned long long *, FrameCounters *, const PolicyState *, cudaStream_t);
-void launch_policy(PolicyState *, const FrameCounters *, FrameRecordDev *, cudaStream_t);
+                 uint32_t *, uint32_t *, uint32_t *, unsigned long long *, FrameCounters *, PolicyState *,
+                 FrameRecordDev *, cudaStream_t);
 void launch_record(const FrameCounters *, FrameRecordDev *, cudaStream_t);
 void launch_margin(int, const float *, const float *, const float *, float4 *, cudaStream_t);
 int cull_tiles(int N);
@@ -88,6 +88,7 @@ struct gsc_ctx {
   // cache
   DevBuf<int32_t> birth;
   DevBuf<uint32_t> vis[2];
+  DevBuf<uint32_t> miss_bits;   // the frame's miss bitset (cull pass 1 -> pass 2)
   int vis_cur = 0;
   DevBuf<float> alpha;
   DevBuf<float4> pool;
@@ -302,6 +303,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   const size_t words = ((size_t)N + 31) / 32 + 1;
   CU(ctx->vis[0].alloc(words));
   CU(ctx->vis[1].alloc(words));
+  CU(ctx->miss_bits.alloc(words));
   CU(ctx->alpha.alloc(NK));
   CU(ctx->pool.alloc(NK * 3));
   CU(cudaMemset(ctx->alpha.p, 0, NK * 4));
@@ -464,9 +466,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   const int cur = ctx->vis_cur;
   // a1 + a2
   launch_cull(fc, ctx->N, ctx->pos_m.p, ctx->level.p, ctx->birth.p, ctx->vis[cur ^ 1].p, ctx->vis[cur].p,
-              ctx->visible.p, ctx->misses.p, reinterpret_cast<unsigned long long *>(S.zero_region.p + ctx->off_cull),
-              ctr, ctx->policy.p, sA);
-  launch_policy(ctx->policy.p, ctr, ctx->rec_dev.p + slot_i, sA);
+              ctx->miss_bits.p, ctx->visible.p, ctx->misses.p, reinterpret_cast<unsigned long long *>(S.zero_region.p + ctx->off_cull),
+              ctr, ctx->policy.p, ctx->rec_dev.p + slot_i, sA);
   mark(sA);
   // a3
   launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p, ctx->b1s.p,

@@ -5,21 +5,24 @@
 //   visible_i = frustum(unified camera, margin m_i) and level_i <= l(d_i),
 //   hit_i     = visible_i and birth_i > W_f          (watermark form of the
 //               explicit eviction "invalidate lines at max reuse depth")
-// with an ordered (ascending-id) compaction of X_f and of the miss list by a
-// single-pass decoupled look-back scan, the visibility bitset of the frame
-// (for |X_f \ X_f-1|) and birth_i = f written for every miss.
+// with an ordered (ascending-id) compaction of X_f and of the miss list as
+// reduce-then-scan over CTA tiles of 4096 anchors: cull_classify writes the
+// frame's visibility bitset (also for |X_f \ X_f-1|), the miss bitset,
+// birth_i = f for every miss and per-tile counts; cull_compact expands the
+// bitsets into the id lists at each tile's prefix.  (A single pass with a
+// decoupled look-back spent ~30% of its stall samples waiting on it.)
 //
 // Layout: pos_m float4[N] = (x, y, z, m_i) -- one 16-byte coalesced load per
-// anchor; level u8[N]; birth i32[N]; bitset u32[ceil(N/32)] (ping-pong).
+// anchor; level u8[N]; birth i32[N]; bitsets u32[ceil(N/32)] (visibility: ping-pong; misses).
 // HBM bytes per anchor: 16 + 1 + 4 + 1/8 (+4 per miss birth write, +4 per
 // visible id, +4 per miss id).
 #include "gsc_internal.cuh"
 
 namespace gsc {
 
-constexpr int kCullThreads = 256;
-constexpr int kCullItems = 4;                                  // per thread
-constexpr int kCullTile = kCullThreads * kCullItems;           // 1024 anchors
+constexpr int kCullThreads = 512;
+constexpr int kCullItems = 8;                                  // per thread
+constexpr int kCullTile = kCullThreads * kCullItems;           // 4096 anchors
 
 __device__ __forceinline__ bool cull_visible(const UniC &u, float4 pm, int level, int L, float d0) {
   float v0 = __fsub_rn(pm.x, u.p[0]), v1 = __fsub_rn(pm.y, u.p[1]), v2 = __fsub_rn(pm.z, u.p[2]);
@@ -41,103 +44,130 @@ __device__ __forceinline__ bool cull_visible(const UniC &u, float4 pm, int level
   return level <= lc;
 }
 
+// Pass 1 (independent tiles): predicates, cache classify, birth update, the frame's visibility and
+// miss bitsets, per-tile (visible, miss) counts -> agg[tile].
 __global__ void __launch_bounds__(kCullThreads)
 cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ pos_m,
                      const uint8_t *__restrict__ level, int32_t *__restrict__ birth,
                      const uint32_t *__restrict__ prev_vis, uint32_t *__restrict__ cur_vis,
-                     uint32_t *__restrict__ visible, uint32_t *__restrict__ misses,
-                     unsigned long long *__restrict__ status, FrameCounters *__restrict__ ctr,
-                     const PolicyState *__restrict__ pol) {
-  __shared__ uint32_t s_tile;
+                     uint32_t *__restrict__ miss_bits, unsigned long long *__restrict__ agg,
+                     FrameCounters *__restrict__ ctr, const PolicyState *__restrict__ pol) {
   __shared__ uint32_t s_wv[kCullThreads / 32], s_wm[kCullThreads / 32];
-  __shared__ unsigned long long s_prefix;
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_cull, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
+  const uint32_t tile = blockIdx.x;
   const int32_t f = pol->frame, W = pol->W;
   const int64_t wbase = (int64_t)tile * kCullTile + warp * (32 * kCullItems);
 
-  uint32_t mv[kCullItems], mm[kCullItems];
+  // all of the thread's anchor loads in flight before the first predicate
+  float4 pm[kCullItems];
+  int lv[kCullItems];
+  int32_t bi[kCullItems];
+#pragma unroll
+  for (int it = 0; it < kCullItems; ++it) {
+    const int64_t i = wbase + it * 32 + lane;
+    pm[it] = i < N ? pos_m[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    lv[it] = i < N ? level[i] : 0;
+    bi[it] = i < N ? birth[i] : 0;
+  }
   uint32_t cnt_v = 0, cnt_m = 0, cnt_new = 0;
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
-    int64_t i = wbase + it * 32 + lane;
+    const int64_t i = wbase + it * 32 + lane;
     bool vis = false, miss = false;
     if (i < N) {
-      float4 pm = pos_m[i];
-      vis = cull_visible(u, pm, level[i], L, d0);
+      vis = cull_visible(u, pm[it], lv[it], L, d0);
       if (vis) {
-        int32_t b = birth[i];
-        miss = !(b > W);
+        miss = !(bi[it] > W);
         if (miss) birth[i] = f;   // derived this frame (Alg. 1 "update computation cache")
       }
     }
-    mv[it] = __ballot_sync(0xFFFFFFFFu, vis);
-    mm[it] = __ballot_sync(0xFFFFFFFFu, miss);
-    int64_t word = (wbase + it * 32) >> 5;
+    const uint32_t mv = __ballot_sync(0xFFFFFFFFu, vis);
+    const uint32_t mm = __ballot_sync(0xFFFFFFFFu, miss);
+    const int64_t word = (wbase + it * 32) >> 5;
     if (wbase + it * 32 < N) {
-      uint32_t pw = prev_vis[word];
-      if (lane == 0) cur_vis[word] = mv[it];
-      cnt_new += __popc(mv[it] & ~pw);
+      const uint32_t pw = prev_vis[word];
+      if (lane == 0) { cur_vis[word] = mv; miss_bits[word] = mm; }
+      cnt_new += __popc(mv & ~pw);
     }
-    cnt_v += __popc(mv[it]);
-    cnt_m += __popc(mm[it]);
+    cnt_v += __popc(mv);
+    cnt_m += __popc(mm);
   }
   if (lane == 0) { s_wv[warp] = cnt_v; s_wm[warp] = cnt_m; }
   if (lane == 0 && cnt_new) atomicAdd(&ctr->n_new, cnt_new);
   __syncthreads();
-
-  // block aggregate and exclusive warp prefixes (warp 0)
-  if (warp == 0) {
-    uint32_t v = lane < kCullThreads / 32 ? s_wv[lane] : 0, m = lane < kCullThreads / 32 ? s_wm[lane] : 0;
-    uint32_t iv = v, im = m;
+  if (threadIdx.x == 0) {
+    uint32_t tv = 0, tm = 0;
 #pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      uint32_t tv = __shfl_up_sync(0xFFFFFFFFu, iv, o), tm = __shfl_up_sync(0xFFFFFFFFu, im, o);
-      if (lane >= (uint32_t)o) { iv += tv; im += tm; }
-    }
-    uint32_t tot_v = __shfl_sync(0xFFFFFFFFu, iv, 31), tot_m = __shfl_sync(0xFFFFFFFFu, im, 31);
-    if (lane < kCullThreads / 32) { s_wv[lane] = iv - v; s_wm[lane] = im - m; }
-    unsigned long long agg = ((unsigned long long)tot_m << 31) | tot_v;
-    if (tile == 0) {
-      if (lane == 0) st_volatile_u64(status, (2ull << 62) | agg);
-      if (lane == 0) s_prefix = 0;
-    } else {
-      if (lane == 0) st_volatile_u64(status + tile, (1ull << 62) | agg);
-      unsigned long long pre = lookback_u64(status, tile);
-      if (lane == 0) {
-        st_volatile_u64(status + tile, (2ull << 62) | (pre + agg));
-        s_prefix = pre;
-      }
-    }
-    uint32_t ntiles = (uint32_t)((N + kCullTile - 1) / kCullTile);
-    if (lane == 0 && tile == ntiles - 1) {
-      unsigned long long pre = (tile == 0) ? 0ull : s_prefix;
-      unsigned long long tot = pre + agg;
-      ctr->n_visible = (uint32_t)(tot & 0x7FFFFFFFull);
-      ctr->n_miss = (uint32_t)((tot >> 31) & 0x7FFFFFFFull);
-    }
+    for (int w = 0; w < kCullThreads / 32; ++w) { tv += s_wv[w]; tm += s_wm[w]; }
+    agg[tile] = ((unsigned long long)tm << 31) | tv;
   }
-  __syncthreads();
-  const unsigned long long pre = s_prefix;
-  uint32_t ov = (uint32_t)(pre & 0x7FFFFFFFull) + s_wv[warp];
-  uint32_t om = (uint32_t)((pre >> 31) & 0x7FFFFFFFull) + s_wm[warp];
-  const uint32_t lt = lanemask_lt();
+}
+
+__device__ __forceinline__ void policy_step(PolicyState *pol, const FrameCounters *ctr, FrameRecordDev *rec);
+
+// Pass 2: ordered (ascending-id) compaction of X_f and of the miss list from the bitsets.  The
+// tile's prefix is the sum of agg[< tile] (L2-resident, read by the whole CTA); warp w expands words
+// [32 w, 32 w + 32) of the tile's 128 bitset words.
+constexpr int kCompThreads = 128;
+__global__ void __launch_bounds__(kCompThreads)
+cull_compact_kernel(int N, const uint32_t *__restrict__ cur_vis, const uint32_t *__restrict__ miss_bits,
+                    const unsigned long long *__restrict__ agg, uint32_t *__restrict__ visible,
+                    uint32_t *__restrict__ misses, FrameCounters *__restrict__ ctr, PolicyState *__restrict__ pol,
+                    FrameRecordDev *__restrict__ rec) {
+  __shared__ unsigned long long s_red[kCompThreads / 32];
+  __shared__ uint32_t s_wv[kCompThreads / 32], s_wm[kCompThreads / 32];
+  const uint32_t t = threadIdx.x, warp = t >> 5, lane = lane_id(), lt = lanemask_lt();
+  const uint32_t tile = blockIdx.x;
+  const uint32_t nwords = (uint32_t)((N + 31) / 32);
+  unsigned long long pre = 0;
+  for (uint32_t j = t; j < tile; j += kCompThreads) pre += agg[j];
 #pragma unroll
-  for (int it = 0; it < kCullItems; ++it) {
-    uint32_t i = (uint32_t)(wbase + it * 32 + lane);
-    if (mv[it] >> lane & 1u) visible[ov + __popc(mv[it] & lt)] = i;
-    if (mm[it] >> lane & 1u) misses[om + __popc(mm[it] & lt)] = i;
-    ov += __popc(mv[it]);
-    om += __popc(mm[it]);
+  for (int o = 16; o > 0; o >>= 1) pre += __shfl_xor_sync(0xFFFFFFFFu, pre, o);
+  const uint32_t word = tile * (kCullTile / 32) + t;
+  const uint32_t mv = word < nwords ? cur_vis[word] : 0u, mm = word < nwords ? miss_bits[word] : 0u;
+  // warp-inclusive scans of the word counts
+  uint32_t iv = __popc(mv), im = __popc(mm);
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t a = __shfl_up_sync(0xFFFFFFFFu, iv, o), b = __shfl_up_sync(0xFFFFFFFFu, im, o);
+    if (lane >= (uint32_t)o) { iv += a; im += b; }
+  }
+  if (lane == 31) { s_wv[warp] = iv; s_wm[warp] = im; }
+  if (lane == 0) s_red[warp] = pre;
+  __syncthreads();
+  unsigned long long tpre = 0;
+  uint32_t ov = 0, om = 0, tv = 0, tm = 0;
+#pragma unroll
+  for (int w = 0; w < kCompThreads / 32; ++w) {
+    tpre += s_red[w];
+    ov += (uint32_t)w < warp ? s_wv[w] : 0u;
+    om += (uint32_t)w < warp ? s_wm[w] : 0u;
+    tv += s_wv[w];
+    tm += s_wm[w];
+  }
+  ov += (uint32_t)(tpre & 0x7FFFFFFFull);
+  om += (uint32_t)((tpre >> 31) & 0x7FFFFFFFull);
+  const uint32_t ntiles = (uint32_t)((N + kCullTile - 1) / kCullTile);
+  if (t == 0 && tile == ntiles - 1) {   // totals, then a2 (n_new is final: pass 1 has completed)
+    ctr->n_visible = (uint32_t)(tpre & 0x7FFFFFFFull) + tv;
+    ctr->n_miss = (uint32_t)((tpre >> 31) & 0x7FFFFFFFull) + tm;
+    policy_step(pol, ctr, rec);
+  }
+  // exclusive offsets of this lane's word; then the warp expands its 32 words one by one
+  uint32_t ev = ov + iv - __popc(mv), em = om + im - __popc(mm);
+  const uint32_t wbase = tile * kCullTile + warp * 1024;
+  for (int j = 0; j < 32; ++j) {
+    const uint32_t v = __shfl_sync(0xFFFFFFFFu, mv, j), m = __shfl_sync(0xFFFFFFFFu, mm, j);
+    const uint32_t bv = __shfl_sync(0xFFFFFFFFu, ev, j), bm = __shfl_sync(0xFFFFFFFFu, em, j);
+    const uint32_t i = wbase + 32 * j + lane;
+    if (v >> lane & 1u) visible[bv + __popc(v & lt)] = i;
+    if (m >> lane & 1u) misses[bm + __popc(m & lt)] = i;
   }
 }
 
 // a2: depth_{f+1} = H(rate), W_{f+1} = max(W_f, f+1 - depth_{f+1}) (Eq. 4; R10).
 // H(num/den) = 1 + floor((2 (D-1)(den - num) + den) / (2 den)); frame 0 keeps D_max.
-__global__ void policy_kernel(PolicyState *pol, const FrameCounters *ctr, FrameRecordDev *rec) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+__device__ __forceinline__ void policy_step(PolicyState *pol, const FrameCounters *ctr, FrameRecordDev *rec) {
   const int32_t f = pol->frame, D = pol->d_max;
   const int32_t depth_used = pol->depth;
   const long long den = ctr->n_visible;
@@ -165,6 +195,11 @@ __global__ void policy_kernel(PolicyState *pol, const FrameCounters *ctr, FrameR
   rec->n_visible = ctr->n_visible;
   rec->n_miss = ctr->n_miss;
   rec->n_new = ctr->n_new;
+}
+// (N = 0 only: otherwise the last cull_compact CTA runs the policy step)
+__global__ void policy_kernel(PolicyState *pol, const FrameCounters *ctr, FrameRecordDev *rec) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  policy_step(pol, ctr, rec);
 }
 
 // final per-frame counts for the host record
@@ -197,16 +232,19 @@ __global__ void margin_kernel(int N, const float *__restrict__ pos, const float 
 }
 
 // ---------------------------------------------------------------- launchers
+// a1 + a2
 void launch_cull(const FrameC &fc, int N, const float4 *pos_m, const uint8_t *level, int32_t *birth,
-                 const uint32_t *prev_vis, uint32_t *cur_vis, uint32_t *visible, uint32_t *misses,
-                 unsigned long long *status, FrameCounters *ctr, const PolicyState *pol, cudaStream_t st) {
+                 const uint32_t *prev_vis, uint32_t *cur_vis, uint32_t *miss_bits, uint32_t *visible,
+                 uint32_t *misses, unsigned long long *agg, FrameCounters *ctr, PolicyState *pol,
+                 FrameRecordDev *rec, cudaStream_t st) {
   int tiles = (N + kCullTile - 1) / kCullTile;
-  if (tiles == 0) return;
+  if (tiles == 0) {
+    policy_kernel<<<1, 32, 0, st>>>(pol, ctr, rec);
+    return;
+  }
   cull_classify_kernel<<<tiles, kCullThreads, 0, st>>>(fc.u, fc.L, fc.d0, N, pos_m, level, birth, prev_vis,
-                                                        cur_vis, visible, misses, status, ctr, pol);
-}
-void launch_policy(PolicyState *pol, const FrameCounters *ctr, FrameRecordDev *rec, cudaStream_t st) {
-  policy_kernel<<<1, 32, 0, st>>>(pol, ctr, rec);
+                                                        cur_vis, miss_bits, agg, ctr, pol);
+  cull_compact_kernel<<<tiles, kCompThreads, 0, st>>>(N, cur_vis, miss_bits, agg, visible, misses, ctr, pol, rec);
 }
 void launch_record(const FrameCounters *ctr, FrameRecordDev *rec, cudaStream_t st) {
   record_kernel<<<1, 32, 0, st>>>(ctr, rec);

@@ -188,6 +188,44 @@ __device__ __forceinline__ uint32_t block_lookback_u32(uint32_t *status, uint32_
   return prefix;
 }
 
+// block_lookback_u32 over 64-bit status words ([63:62] flag, [61:0] two packed counts, see below):
+// one round trip covers kThreads predecessors.  All threads call it; `red` is kThreads/32 + 1 u64
+// words of shared scratch.
+template <int kThreads>
+__device__ __forceinline__ unsigned long long block_lookback_u64(unsigned long long *status, uint32_t tile,
+                                                                 unsigned long long *red) {
+  constexpr unsigned long long kMask = (1ull << 62) - 1;
+  constexpr int kW = kThreads / 32;
+  const uint32_t t = threadIdx.x, lane = t & 31u, warp = t >> 5;
+  unsigned long long prefix = 0;
+  int64_t base = (int64_t)tile - 1;
+  while (base >= 0) {
+    const int64_t idx = base - (int64_t)t;
+    unsigned long long s = 2ull << 62;   // out of range counts as an inclusive zero
+    if (idx >= 0) {
+      do { s = ld_volatile_u64(status + idx); } while ((s >> 62) == 0);
+    }
+    const uint32_t incl = __ballot_sync(0xFFFFFFFFu, (s >> 62) == 2ull);
+    if (lane == 0) red[warp] = incl ? warp * 32 + (uint32_t)(__ffs(incl) - 1) : (uint32_t)kThreads;
+    __syncthreads();
+    uint32_t upto = kThreads;
+#pragma unroll
+    for (int w = 0; w < kW; ++w) upto = min(upto, (uint32_t)red[w]);
+    unsigned long long v = t <= upto ? (s & kMask) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xFFFFFFFFu, v, o);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+#pragma unroll
+    for (int w = 0; w < kW; ++w) prefix += red[w];
+    __syncthreads();
+    if (upto < (uint32_t)kThreads) break;
+    base -= kThreads;
+  }
+  return prefix;
+}
+
 // 64-bit status: [63:62] flag, [61:31] field b, [30:0] field a (two counts).
 __device__ __forceinline__ unsigned long long lookback_u64(unsigned long long *status, uint32_t tile) {
   constexpr unsigned long long kMask = (1ull << 62) - 1;
