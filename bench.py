@@ -135,8 +135,9 @@ def run_gsc(args):
     traj = sg.trajectory(cfg)
     fmt = gp.GSC_FMT_RGBA8
     free0 = torch.cuda.mem_get_info(dev)[0]
+    base = gp.GSC_F_STAGGER if args.stagger else 0   # the F3 variant (R26); 0 = the method
     r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
-                    flags=0, pair_capacity=args.pair_capacity).load(sc)
+                    flags=base, pair_capacity=args.pair_capacity).load(sc)
     torch.cuda.synchronize()
     mem_bytes = free0 - torch.cuda.mem_get_info(dev)[0]   # the context's device memory (scene, cache, frames)
     out_l, out_r = r.alloc_outputs(fmt)
@@ -194,7 +195,7 @@ def run_gsc(args):
     # timed run counts)
     def replay(flags):
         r.reset_cache()
-        r.set_flags(flags)
+        r.set_flags(flags | base)
         r.stats_history()
         for f in frames:
             r.render_into(traj[f], out_l, out_r, fmt, stream)
@@ -202,7 +203,7 @@ def run_gsc(args):
         return r.stats_history(max(args.steps, 1))
     staged = replay(gp.GSC_F_STAGE_TIMING | gp.GSC_F_SERIAL)
     counted = replay(gp.GSC_F_COUNT_EVALS)
-    r.set_flags(0)
+    r.set_flags(base)
 
     total_frames = world * len(frames)
     value = total_frames / (t_max / 1000.0) if t_max > 0 else 0.0
@@ -269,7 +270,8 @@ def run_gsc(args):
                        "anchors": sc.n, "width": cfg.width, "height": cfg.height, "d_max": cfg.d_max,
                        "frames_per_rank": len(frames), "out_format": "rgba8",
                        "l2": "no flush: per-frame working set (pool/splat/pair traffic ~1-2 GB) > 126 MB L2",
-                       "parallelism": f"frames partitioned by view, scene replicated, dp{world}"},
+                       "parallelism": f"frames partitioned by view, scene replicated, dp{world}",
+                       **({"variant": "staggered expiry (GSC_F_STAGGER, F3)"} if args.stagger else {})},
             "stages": stage_report,
             "stages_note": "CUDA events per stage in a replay of the same frames with GSC_F_SERIAL (no overlap of "
                            "frame f+1's front end with frame f's blend); the timed run overlaps them on two streams",
@@ -366,6 +368,7 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C2", "C3", "C4", "C5"])
     ap.add_argument("--pair-capacity", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stagger", action="store_true", help="staggered expiry variant (GSC_F_STAGGER, SURVEY 8(f) F3)")
     ap.add_argument("--cpu-sample-frames", type=int, default=1)
     ap.add_argument("--ref-frames", type=int, default=4)
     args = ap.parse_args()

@@ -76,6 +76,12 @@ typedef struct gsc_ctx gsc_ctx;
 #define GSC_F_MONO 0x200u           /* render the left eye only (the right image is left untouched); with a
                                         rig whose eyes coincide this is a monocular pipeline -- two such
                                         contexts, one per eye, are the no-de-redundancy ablation (F1) */
+#define GSC_F_STAGGER 0x400u        /* staggered expiry (R26): an anchor derived
+                                       for the first time since the last reset at frame f is given birth
+                                       f - min(i mod D_max, f - 1 - W_f), so lines filled together (the
+                                       first frame) expire spread over D_max frames, not all at once
+                                       (no periodic full re-derivation spikes).  Applies from the next
+                                       gsc_reset_cache / load */
 #define GSC_F_SERIAL 0x10u       /* do not overlap frame f+1's front end (cull .. ranges) with frame f's
                                     blend: per-stage times then add up to the frame time */
 

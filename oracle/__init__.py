@@ -64,7 +64,7 @@ class Config(C.Structure):
     _fields_ = [("width", C.c_int), ("height", C.c_int), ("fov_y", C.c_double),
                 ("near_plane", C.c_double), ("far_plane", C.c_double), ("bg", C.c_float * 3),
                 ("d_max", C.c_int), ("depth_literal", C.c_int), ("guide", C.c_int),
-                ("ablate", C.c_int)]
+                ("ablate", C.c_int), ("stagger", C.c_int)]
 
 
 class Eye(C.Structure):
@@ -164,7 +164,7 @@ def elem(fn: str, x) -> np.ndarray:
 
 
 def make_config(width, height, fov_y_deg=70.0, near=0.05, far=5000.0, d_max=10, bg=(0, 0, 0),
-                depth_literal=False, guide=0, ablate=0) -> Config:
+                depth_literal=False, guide=0, ablate=0, stagger=False) -> Config:
     c = Config()
     c.width, c.height = width, height
     c.fov_y = np.deg2rad(fov_y_deg)
@@ -175,6 +175,7 @@ def make_config(width, height, fov_y_deg=70.0, near=0.05, far=5000.0, d_max=10, 
     c.depth_literal = int(depth_literal)
     c.guide = int(guide)       # 0 linear, 1 exponential, 2 staged (R23)
     c.ablate = int(ablate)     # ORC_ABL_* bits: 1 fixed 3-sigma extent, 2 AABB tiles (F1 ablations)
+    c.stagger = int(bool(stagger))   # staggered expiry (F3, R26)
     return c
 
 

@@ -523,12 +523,15 @@ void orc_blend_pixel(const orc_splat *const *list, int n, float pxc, float pyc, 
 /* ======================================================================
  * Whole-frame state machine (Alg. 1).
  * ====================================================================== */
+#define ORC_EMPTY INT32_MIN   /* birth of an empty cache line */
 struct orc_state {
   orc_scene sc;
   orc_config cfg;
   int64_t frame;
   int depth;
-  int32_t *birth;       /* -1 = empty (explicit eviction) */
+  int32_t *birth;       /* ORC_EMPTY = empty (explicit eviction) */
+  uint8_t *ever;        /* anchor derived at least once since the last reset (staggered expiry) */
+  int64_t W;            /* W_f = max_{f' <= f} (f' - depth_f'), W_0 = -D_max (staggered expiry cap) */
   uint8_t *prev_vis, *cur_vis;
   float *margin;
   float *alpha, *mu, *cov, *rgb;    /* pool, slot g = i*K + j */
@@ -549,6 +552,7 @@ orc_state *orc_create(const orc_scene *sc, const orc_config *cfg) {
   st->cfg = *cfg;
   size_t N = (size_t)sc->N;
   st->birth = (int32_t *)malloc(N * sizeof(int32_t));
+  st->ever = (uint8_t *)calloc(N, 1);
   st->prev_vis = (uint8_t *)calloc(N, 1);
   st->cur_vis = (uint8_t *)calloc(N, 1);
   st->margin = (float *)malloc(N * sizeof(float));
@@ -569,14 +573,16 @@ void orc_reset(orc_state *st) {
   size_t N = (size_t)st->sc.N;
   st->frame = 0;
   st->depth = st->cfg.d_max;            /* Alg. 1 */
-  for (size_t i = 0; i < N; ++i) st->birth[i] = -1;
+  st->W = -(int64_t)st->cfg.d_max;
+  for (size_t i = 0; i < N; ++i) st->birth[i] = ORC_EMPTY;
+  memset(st->ever, 0, N);
   memset(st->prev_vis, 0, N);
   st->n_visible = st->n_misses = 0;
 }
 
 void orc_destroy(orc_state *st) {
   if (!st) return;
-  free(st->birth); free(st->prev_vis); free(st->cur_vis); free(st->margin);
+  free(st->birth); free(st->ever); free(st->prev_vis); free(st->cur_vis); free(st->margin);
   free(st->alpha); free(st->mu); free(st->cov); free(st->rgb);
   free(st->visible); free(st->misses);
   for (int e = 0; e < 2; ++e) { free(st->spl[e]); free(st->spl_g[e]); }
@@ -616,7 +622,7 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
 
   /* Alg. 1 l.185-187: invalidate lines at max reuse depth (explicit eviction) */
   for (int i = 0; i < N; ++i)
-    if (st->birth[i] >= 0 && f - st->birth[i] >= depth) st->birth[i] = -1;
+    if (st->birth[i] != ORC_EMPTY && f - st->birth[i] >= depth) st->birth[i] = ORC_EMPTY;
 
   /* Alg. 1 l.184 anchors indexing and filtering, through the unified camera */
 #pragma omp parallel for schedule(static)
@@ -627,7 +633,7 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
     if (!st->cur_vis[i]) continue;
     st->visible[nv++] = (uint32_t)i;
     if (!st->prev_vis[i]) ++nnew;
-    if (st->birth[i] < 0) st->misses[nm++] = (uint32_t)i;   /* hit <=> live cache line */
+    if (st->birth[i] == ORC_EMPTY) st->misses[nm++] = (uint32_t)i;   /* hit <=> live cache line */
   }
   st->n_visible = nv;
   st->n_misses = nm;
@@ -639,7 +645,20 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
     size_t g0 = (size_t)i * K;
     orc_derive_anchor(sc, i, u.p, st->alpha + g0, st->mu + 3 * g0, st->cov + 6 * g0, st->rgb + 3 * g0, NULL);
   }
-  for (int m = 0; m < nm; ++m) st->birth[st->misses[m]] = (int32_t)f;
+  /* update computation cache: the line of a derived anchor is born now.  Staggered expiry (F3, R26):
+   * a never-derived anchor's line is back-dated by s_i = min(i mod D_max, f - 1 - W_f) frames, so the
+   * lines filled together on a cold frame expire spread over D_max frames instead of all at once;
+   * the cap keeps birth > W_f (the line is live until its own age reaches the depth). */
+  for (int m = 0; m < nm; ++m) {
+    const uint32_t i = st->misses[m];
+    int64_t b = f;
+    if (cfg->stagger && !st->ever[i]) {
+      int64_t s = (int64_t)(i % (uint32_t)cfg->d_max), cap = f - 1 - st->W;
+      b = f - (s < cap ? s : cap);
+    }
+    st->birth[i] = (int32_t)b;
+    st->ever[i] = 1;
+  }
 
   /* Alg. 1 l.198: depth <- H(rate); R10: rate = novelty |X_f \ X_f-1| / |X_f|
    * (SPEC-literal alternative: miss rate). Frame 0 keeps D_max. */
@@ -652,6 +671,7 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
     stats->depth_used = depth; stats->depth_next = depth_next;
   }
   st->depth = depth_next;
+  if ((f + 1) - depth_next > st->W) st->W = (f + 1) - depth_next;   /* W_{f+1} */
   uint8_t *tmp = st->prev_vis; st->prev_vis = st->cur_vis; st->cur_vis = tmp;
   st->frame = f + 1;
 

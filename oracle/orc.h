@@ -54,6 +54,9 @@ typedef struct {
   int depth_literal; /* 1: SPEC-literal H(miss rate); 0: H(novelty) */
   int guide;         /* guiding function H: ORC_GUIDE_LINEAR (default), _EXP, _STAGED (R23) */
   int ablate;        /* ORC_ABL_* bits (SURVEY §8(f) F1 ablations of P:256; 0 = the method) */
+  int stagger;       /* 1: staggered expiry (R26): a never-derived anchor
+                        missed at frame f gets birth f - min(i mod D_max, f - 1 - W_f), so the lines
+                        filled together (first frame) expire spread over D_max frames */
 } orc_config;
 
 #define ORC_ABL_FIXED_EXTENT 1  /* extent r^2 = 9 (fixed 3 sigma) instead of 2 ln(255 alpha) */

@@ -371,6 +371,7 @@ static gsc_status reset_cache(gsc_ctx *ctx, cudaStream_t st) {
   ps.d_max = ctx->cfg.d_max;
   ps.literal = (ctx->cfg.flags & GSC_F_DEPTH_LITERAL) ? 1 : 0;
   ps.guide = (ctx->cfg.flags & GSC_F_GUIDE_EXP) ? 1 : (ctx->cfg.flags & GSC_F_GUIDE_STAGED) ? 2 : 0;
+  ps.stagger = (ctx->cfg.flags & GSC_F_STAGGER) ? 1 : 0;
   CU(cudaMemcpyAsync(ctx->policy.p, &ps, sizeof(ps), cudaMemcpyHostToDevice, st));
   CU(cudaStreamSynchronize(st));
   return GSC_OK;
@@ -701,7 +702,7 @@ gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
   if (!ctx) return GSC_EINVAL;
   const unsigned known =
       GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL |
-      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES | GSC_F_MONO;
+      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES | GSC_F_MONO | GSC_F_STAGGER;
   if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
   if ((flags & GSC_F_GUIDE_EXP) && (flags & GSC_F_GUIDE_STAGED)) return fail(ctx, GSC_EINVAL, "two guiding functions");
   CU(cudaSetDevice(ctx->device));

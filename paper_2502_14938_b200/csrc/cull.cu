@@ -78,7 +78,16 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
       vis = cull_visible(u, pm[it], lv[it], L, d0);
       if (vis) {
         miss = !(bi[it] > W);
-        if (miss) birth[i] = f;   // derived this frame (Alg. 1 "update computation cache")
+        // derived this frame (Alg. 1 "update computation cache"); GSC_F_STAGGER (R26): a line filled
+        // for the first time since the reset (birth INT32_MIN) is back-dated by min(i mod D, f-1-W)
+        if (miss) {
+          int32_t b = f;
+          if (pol->stagger && bi[it] == INT32_MIN) {
+            const int32_t s = (int32_t)((uint32_t)i % (uint32_t)pol->d_max), cap = f - 1 - W;
+            b = f - (s < cap ? s : cap);
+          }
+          birth[i] = b;
+        }
       }
     }
     const uint32_t mv = __ballot_sync(0xFFFFFFFFu, vis);

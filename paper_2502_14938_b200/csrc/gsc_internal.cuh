@@ -61,7 +61,8 @@ struct PolicyState {
   int32_t d_max;
   int32_t literal;     // GSC_F_DEPTH_LITERAL
   int32_t guide;       // guiding function: 0 linear, 1 exponential, 2 staged (GSC_F_GUIDE_*)
-  int32_t pad[2];
+  int32_t stagger;     // GSC_F_STAGGER (R26)
+  int32_t pad;
 };
 
 // compacted splat records (index c), written by project, read by emit/blend

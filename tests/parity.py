@@ -17,10 +17,10 @@ def psnr(a, b):
     return float("inf") if mse == 0 else 10 * np.log10(1.0 / mse)
 
 
-def oracle_config(orc, cfg, d_max=None, literal=False, guide=0, ablate=0):
+def oracle_config(orc, cfg, d_max=None, literal=False, guide=0, ablate=0, stagger=False):
     return orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far,
                            cfg.d_max if d_max is None else d_max, depth_literal=literal, guide=guide,
-                           ablate=ablate)
+                           ablate=ablate, stagger=stagger)
 
 
 def renderer(cfg, d_max=None, flags=0, pair_capacity=0):

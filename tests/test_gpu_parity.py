@@ -77,6 +77,32 @@ def test_c1_moving_trajectory_cache(orc, c1):
         _frame_parity(orc, o, r, rig)
 
 
+@pytest.mark.parametrize("d_max", [4, 10])
+def test_c1_staggered_expiry(orc, c1, d_max):
+    """GSC_F_STAGGER (F3, R26): static frames (one D-th of the anchors re-derived per frame, no
+    flush frame), then a moving stretch: hit/miss sets and depths every frame, births of the
+    visible anchors, full parity on some frames."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg, d_max=d_max, stagger=True))
+    r = renderer(cfg, d_max=d_max, flags=gp.GSC_F_STAGGER).load(sc)
+    c = cfg.center
+    rig0 = sg.trajectory(cfg)[0]
+    for f in range(28):
+        if f < 2 * d_max:
+            rig = rig0
+        else:
+            eye = c + np.array([25 * np.cos(0.12 * f), 25 * np.sin(0.12 * f), 2.0 + 0.5 * f])
+            rig = sg.look_at_rig(eye, c + np.array([0, 0, 3.0]), 0.064)
+        st, _ = _frame_parity(orc, o, r, rig, full=(f % 5 == 0))
+        if 0 < f < 2 * d_max:
+            assert 0 < st["n_misses"] < st["n_visible"] // 2
+        vis = r.debug("visible")
+        birth = r.debug("birth")
+        for i in vis[::29]:
+            assert birth[i] == o.birth(int(i))
+
+
 @pytest.mark.parametrize("guide", [1, 2])
 def test_c1_guide_variants(orc, c1, guide):
     """Exponential / staged guiding functions (GSC_F_GUIDE_EXP / _STAGED, R23) over a moving

@@ -76,9 +76,9 @@ def test_guide_variants_drive_the_state_machine(orc, c1):
 
 
 # ---------------------------------------------------------------- state machine
-def _oracle(orc, cfg, sc, d_max=None, literal=False):
+def _oracle(orc, cfg, sc, d_max=None, literal=False, stagger=False):
     oc = orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far,
-                         cfg.d_max if d_max is None else d_max, depth_literal=literal)
+                         cfg.d_max if d_max is None else d_max, depth_literal=literal, stagger=stagger)
     return orc.Oracle(sc, oc)
 
 
@@ -100,6 +100,30 @@ def test_static_pose_reuse_and_flush(orc, c1):
             assert st.n_misses == st.n_visible
         else:
             assert st.n_misses == 0
+
+
+@pytest.mark.parametrize("d_max", [4, 10])
+def test_staggered_expiry_static_pose(orc, c1, d_max):
+    """Staggered expiry (F3, R26) under a static camera (novelty 0, depth stays D): frame 0 derives
+    every visible anchor, back-dating anchor i by s_i = i mod D (W_0 = -D, so the cap D - 1 does not
+    bind); the line then lives D - s_i frames, and from then on every D frames.  So frame f >= 1
+    re-derives exactly the visible anchors with i = -f (mod D) -- one D-th of them -- instead of all
+    of them every D frames (test_static_pose_reuse_and_flush)."""
+    cfg, sc = c1
+    o = _oracle(orc, cfg, sc, d_max=d_max, stagger=True)
+    rig = sg.trajectory(cfg)[0]
+    for f in range(3 * d_max + 2):
+        st = o.frame(rig, raster=False).stats
+        vis = o.visible()
+        if f == 0:
+            assert st.n_misses == st.n_visible > 0
+            for i in vis[::53]:
+                assert o.birth(int(i)) == -(int(i) % d_max)
+        else:
+            assert np.array_equal(o.misses(), vis[vis % d_max == (-f) % d_max])
+            assert st.depth_next == d_max
+            for i in o.misses()[::17]:
+                assert o.birth(int(i)) == f
 
 
 def test_dmax1_decodes_every_frame(orc, c1):
@@ -139,22 +163,28 @@ def _moving_rigs(cfg, n, seed):
     return rigs
 
 
-@pytest.mark.parametrize("seed", [1, 2, 3])
-def test_watermark_equals_explicit_eviction(orc, c1, seed):
+@pytest.mark.parametrize("seed,stagger", [(1, False), (2, False), (3, False), (1, True), (2, True)])
+def test_watermark_equals_explicit_eviction(orc, c1, seed, stagger):
     """The GPU's rule hit <=> birth > W_f, W_f = max_f'<=f (f' - depth_f'), no
     eviction writes, equals the oracle's explicit
-    eviction on every frame of a random trajectory."""
+    eviction on every frame of a random trajectory -- also with staggered
+    expiry (R26), whose back-dating cap f - 1 - W_f is what keeps the two forms equal."""
     cfg, sc = c1
-    o = _oracle(orc, cfg, sc, d_max=4)
-    birth = np.full(sc.n, np.iinfo(np.int32).min, np.int64)
-    W = np.iinfo(np.int64).min
+    o = _oracle(orc, cfg, sc, d_max=4, stagger=stagger)
+    empty = np.iinfo(np.int32).min
+    birth = np.full(sc.n, empty, np.int64)
+    W = -4
     for f, rig in enumerate(_moving_rigs(cfg, 60, seed)):
         st = o.frame(rig, raster=False).stats
         W = max(W, f - st.depth_used)
         vis = o.visible()
         miss_w = vis[~(birth[vis] > W)]
         assert np.array_equal(miss_w, o.misses())
-        birth[miss_w] = f
+        new = np.full(len(miss_w), f, np.int64)
+        if stagger:
+            cold = birth[miss_w] == empty
+            new[cold] = f - np.minimum(miss_w[cold].astype(np.int64) % 4, f - 1 - W)
+        birth[miss_w] = new
         for i in vis[::37]:
             assert (o.birth(int(i)) == birth[i])
 

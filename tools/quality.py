@@ -65,6 +65,7 @@ def run(config="C3", frames=150):
         "method": (cfg.d_max, 0),
         "guide_exponential": (cfg.d_max, gp.GSC_F_GUIDE_EXP),
         "guide_staged": (cfg.d_max, gp.GSC_F_GUIDE_STAGED),
+        "stagger": (cfg.d_max, gp.GSC_F_STAGGER),         # staggered expiry (F3, R26)
         "abl_fixed_extent": (cfg.d_max, gp.GSC_F_ABL_FIXED_EXTENT),
         "abl_aabb_tiles": (cfg.d_max, gp.GSC_F_ABL_AABB_TILES),
         "no_reuse": (1, 0),
