@@ -37,7 +37,17 @@ __device__ __forceinline__ bool cull_visible(const UniC &u, float4 pm, int level
   if (d2 == 0.0f) {
     lc = L - 1;
   } else {
-    int e = ilogb_bits(__fdiv_rn(d0, __fsqrt_rn(d2)));
+    // e = ilogb(fl(d0 / fl(sqrt(d2)))) (R9, same op sequence as the oracle).  N9 fast path:
+    // y = d0 * rsqrt.approx(d2) is within a few ulps of that quotient, so when y's mantissa is more
+    // than 2^8 ulps away from both binade edges the exponent field of y is the exact e; only the
+    // rest (and d2 outside the normal range of the approximation) takes the IEEE divide + sqrt.
+    int e;
+    const uint32_t yb = __float_as_uint(__fmul_rn(d0, rsqrtf(d2)));
+    const uint32_t ym = yb & 0x7FFFFFu, yx = yb >> 23;
+    if (d2 >= 1e-30f && d2 <= 1e30f && ym > 256u && ym < 0x7FFFFFu - 256u && yx - 1u < 253u)
+      e = (int)yx - 127;
+    else
+      e = ilogb_bits(__fdiv_rn(d0, __fsqrt_rn(d2)));
     long long l = (long long)e + (L - 1);
     lc = (int)(l < 0 ? 0 : (l > L - 1 ? L - 1 : l));
   }
