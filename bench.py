@@ -259,7 +259,9 @@ def run_gsc(args):
         cpu = cpu_baseline(cfg, sc, traj, frames[:max(1, args.cpu_sample_frames)])
 
     if rank == 0:
-        launches_per_frame = 14
+        # cull_classify, cull_compact, derive_mma, live, project, 4 depth passes, pairoff_reduce,
+        # pairoff_scan, expand, 2 tile passes, blend, record
+        launches_per_frame = 16
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": len(frames),
             "warmup": args.warmup, "ms_per_step": round(t_max / max(1, len(frames)), 4),
