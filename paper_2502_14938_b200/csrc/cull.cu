@@ -8,7 +8,8 @@
 // with an ordered (ascending-id) compaction of X_f and of the miss list as
 // reduce-then-scan over CTA tiles of 4096 anchors: cull_classify writes the
 // frame's visibility bitset (also for |X_f \ X_f-1|), the miss bitset,
-// birth_i = f for every miss and per-tile counts; cull_compact expands the
+// birth_i = f for every miss (back-dated under GSC_F_STAGGER, R26) and
+// per-tile counts; cull_compact expands the
 // bitsets into the id lists at each tile's prefix.  (A single pass with a
 // decoupled look-back spent ~30% of its stall samples waiting on it.)
 //
