@@ -30,8 +30,7 @@ constexpr int kSTile = kSThreads * kSItems;   // 4096 keys
 constexpr int kBins = 256;
 
 struct SortSmem {
-  uint32_t keys[kSTile];
-  uint32_t vals[kSTile];
+  uint2 kv[kSTile];                      // (key, value) interleaved: one 64-bit SMEM access per element
   uint32_t whist[kSWarps][kBins + 4];   // per-warp counts -> exclusive prefixes (bin 256 = invalid)
   uint32_t match[kSWarps][kBins + 4];   // per-warp lane masks of the current item's digit (kept zero)
   uint32_t blk_off[kBins];
@@ -163,7 +162,14 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
       __syncthreads();
       uint32_t wp = 0;
       for (uint32_t w = 0; w < warp; ++w) wp += s_w2[w];
-      S.blk_off[d] = wp + inc - run;
+      const uint32_t boff = wp + inc - run;
+      S.blk_off[d] = boff;
+      // fold the digit's block offset into the per-warp prefixes and its global base, so the scatter
+      // and the write-out each read one digit-indexed word per element instead of two (the digit-
+      // indexed SMEM reads are the bank-conflicted ones; the kernel is bound by the L1/SMEM pipe)
+#pragma unroll 1
+      for (int w = 0; w < kSWarps; ++w) S.whist[w][d] += boff;
+      S.gbase[d] -= boff;
     }
     __syncthreads();
 
@@ -173,24 +179,24 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
       uint32_t idx = wbase + i * 32 + lane;
       if (idx < n) {
         uint32_t d = (key[i] >> shift) & dmask;
-        uint32_t pos = S.blk_off[d] + S.whist[warp][d] + rank[i];
-        S.keys[pos] = key[i];
-        S.vals[pos] = kIota ? idx : vals_in[idx];
+        uint32_t pos = S.whist[warp][d] + rank[i];
+        S.kv[pos] = make_uint2(key[i], kIota ? idx : vals_in[idx]);
       }
     }
     __syncthreads();
     const uint32_t nvalid = min((uint32_t)kSTile, n - tile * kSTile);
     for (uint32_t i = t; i < nvalid; i += kSThreads) {
-      uint32_t k = S.keys[i];
+      const uint2 e = S.kv[i];
+      const uint32_t k = e.x;
       uint32_t d = (k >> shift) & dmask;
-      uint32_t o = S.gbase[d] + (i - S.blk_off[d]);
+      uint32_t o = S.gbase[d] + i;
       keys_out[o] = k;
-      vals_out[o] = S.vals[i];
+      vals_out[o] = e.y;
       if (kRanges) {
         constexpr uint32_t kM = 0x00FFFFFFu;   // tile key (bits 24..31: blend block mask)
         const uint32_t tk = k & kM;
-        const bool first = i == 0 || (S.keys[i - 1] & kM) != tk;
-        const bool last = i + 1 == nvalid || (S.keys[i + 1] & kM) != tk;
+        const bool first = i == 0 || (S.kv[i - 1].x & kM) != tk;
+        const bool last = i + 1 == nvalid || (S.kv[i + 1].x & kM) != tk;
         if (first) atomicMax(&ranges[tk].x, ~o);
         if (last) atomicMax(&ranges[tk].y, o + 1);
       }
