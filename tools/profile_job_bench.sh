@@ -1,0 +1,12 @@
+# Final-kernel refresh (run from the repo root on the GPU box): GPU tests, smoke, bench lines, launch list,
+# one-frame ncu capture.  Outputs under gpurun_out/prof2/.
+set -x
+mkdir -p gpurun_out/prof2
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/prof2/smoke.txt 2>&1
+timeout 1200 python -m pytest tests -q -m gpu > gpurun_out/prof2/pytest_gpu.txt 2>&1
+python bench.py --steps 600 --warmup 5 > gpurun_out/prof2/bench_C4.txt 2>&1
+python bench.py --steps 600 --warmup 5 --no-cpu-baseline --stagger > gpurun_out/prof2/bench_C4_stagger.txt 2>&1
+python bench.py --config C5 --steps 600 --warmup 5 --no-cpu-baseline > gpurun_out/prof2/bench_C5.txt 2>&1
+GSC_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 300 --warmup 5 --no-cpu-baseline > gpurun_out/prof2/bench_2rank.txt 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/prof2/launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline > gpurun_out/prof2/ncu_launch_run.txt 2>&1
+ncu --set full --clock-control none --import-source on -s 1600 -c 16 -o gpurun_out/prof2/frame100 python bench.py --steps 110 --warmup 3 --no-cpu-baseline > gpurun_out/prof2/ncu_full_run.txt 2>&1
