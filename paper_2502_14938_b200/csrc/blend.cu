@@ -62,7 +62,9 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const bool inside = px < fc.width && py < fc.height;
   const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
   // ranges hold (~start, end) (sort.cu, last tile pass); an untouched tile (0, 0) is empty
-  const uint2 rg = make_uint2(~ranges[tile].x, ranges[tile].y);
+  uint2 rg = make_uint2(~ranges[tile].x, ranges[tile].y);
+  rg.x = __shfl_sync(0xFFFFFFFFu, rg.x, 0);   // (uniform by construction; tells the compiler)
+  rg.y = __shfl_sync(0xFFFFFFFFu, rg.y, 0);
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
   // a lane's liveness floor on power: -inf while it composites, +inf once it has terminated (or lies
   // outside the image), so nothing is live for it any more (one FMNMX instead of a predicate chain)
@@ -94,7 +96,8 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     const bool done0 = pfloor > 0.0f;
     uint32_t pstop = end;
 #pragma unroll 2
-    for (uint32_t p = base; p < end; p += 16) {   // warp-uniform trip count
+    for (uint32_t j = 0; j < n; ++j) {   // warp-uniform trip count
+      const uint32_t p = base + 16 * j;
       const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
       const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
       const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
