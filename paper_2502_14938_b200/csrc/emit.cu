@@ -141,9 +141,12 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   for (int k = threadIdx.x; k < 512; k += kXThreads) (&s_hist[0][0])[k] = 0;
   __syncthreads();
   const uint32_t lane = lane_id();
-  const uint32_t P = ctr->n_pairs, C = ctr->n_splat;
+  // (P, C and the warp index broadcast from lane 0: warp-uniform by construction, and visibly so to
+  // the compiler, which then drops the convergence checks around the searches' ballots)
+  const uint32_t P = __shfl_sync(0xFFFFFFFFu, ctr->n_pairs, 0), C = __shfl_sync(0xFFFFFFFFu, ctr->n_splat, 0);
   const uint32_t nchunks = (P + kExpChunk - 1) / kExpChunk;
-  const uint32_t gw = (blockIdx.x * kXThreads + threadIdx.x) >> 5, nw = (gridDim.x * kXThreads) >> 5;
+  const uint32_t gw = __shfl_sync(0xFFFFFFFFu, (blockIdx.x * kXThreads + threadIdx.x) >> 5, 0);
+  const uint32_t nw = (gridDim.x * kXThreads) >> 5;
   for (uint32_t ch = gw; ch < nchunks; ch += nw) {
     const uint32_t q0 = ch * kExpChunk, q1 = min(q0 + kExpChunk, P) - 1;
     const uint32_t pa = warp_find(in.pair_off, C, q0), pb = warp_find(in.pair_off, C, q1);

@@ -390,14 +390,17 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
   WarpRows &ws = s_wr[warp];
   for (int k = threadIdx.x; k < 4 * 256; k += kPThreads) (&s_hist[0][0])[k] = 0;
   __syncthreads();
-  const uint32_t n_live = ctr->n_splat / 2;
+  // (n_live and the warp's first item broadcast from lane 0: warp-uniform by construction, and visibly
+  // so to the compiler, which then drops the convergence checks around the walk's warp collectives)
+  const uint32_t n_live = __shfl_sync(0xFFFFFFFFu, ctr->n_splat / 2, 0);
   const uint32_t nw = (gridDim.x * kPThreads) >> 5;
+  const uint32_t base0 = __shfl_sync(0xFFFFFFFFu, ((blockIdx.x * kPThreads) >> 5) * 16 + warp * 16, 0);
   uint32_t pairs_local = 0;
   // lane = (item, eye): 16 live Gaussians per warp step, lanes 2k / 2k+1 take Gaussian k's left / right
   // eye (half the per-thread state of a lane doing both eyes: more warps in flight)
   const uint32_t e = lane & 1u;
   const EyeC &ec = e ? fc.eye[1] : fc.eye[0];
-  for (uint32_t base = ((blockIdx.x * kPThreads) >> 5) * 16 + warp * 16; base < n_live; base += nw * 16) {
+  for (uint32_t base = base0; base < n_live; base += nw * 16) {
     const uint32_t i = base + (lane >> 1);
     const bool valid = i < n_live;
     SplatOut o;
