@@ -237,7 +237,7 @@ def run_gsc(args):
                 "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4), "traffic": None,
                 "note": f"algorithmic bytes/frame {algo[dom] / nf:.4g}; peak {peaks['src']}"}
     # DRAM traffic of the dominant kernel from the committed ncu --set full capture
-    kernels = {"blend": ["blend_kernel"], "project": ["live_kernel", "project_kernel"], "cull": ["cull_classify_kernel", "cull_compact_kernel"],
+    kernels = {"blend": ["blend_kernel"], "project": ["live_mark_kernel", "live_kernel", "project_kernel"], "cull": ["cull_classify_kernel", "cull_compact_kernel"],
                "derive": ["derive_mma_kernel"], "depth_sort": ["onesweep_pass_kernel"] * 4,
                "tile_sort": ["onesweep_pass_kernel"] * 2, "emit": ["pairoff_kernel", "expand_kernel"],
                "ranges": []}
@@ -259,9 +259,9 @@ def run_gsc(args):
         cpu = cpu_baseline(cfg, sc, traj, frames[:max(1, args.cpu_sample_frames)])
 
     if rank == 0:
-        # cull_classify, cull_compact, derive_mma, live, project, 4 depth passes, pairoff_reduce,
+        # cull_classify, cull_compact, derive_mma, live_mark, live, project, 4 depth passes, pairoff_reduce,
         # pairoff_scan, expand, 2 tile passes, blend, record
-        launches_per_frame = 16
+        launches_per_frame = 17
         line = {
             "metric": METRIC, "value": round(value, 3), "unit": UNIT, "n_gpus": world, "steps": len(frames),
             "warmup": args.warmup, "ms_per_step": round(t_max / max(1, len(frames)), 4),

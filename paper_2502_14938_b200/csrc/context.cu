@@ -27,7 +27,8 @@ int cull_tiles(int N);
 void launch_derive(const float pu[3], const uint32_t *, const float4 *, const int8_t *, const float *, const float *,
                    const int8_t *, const int32_t *, const int8_t *, const int32_t *, float *, float4 *,
                    FrameCounters *, int, bool, cudaStream_t);
-void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, uint32_t *, const SplatBufs &,
+void launch_project(const FrameC &, const uint32_t *, const float *, const float4 *, uint32_t *, uint32_t *,
+                    const SplatBufs &,
                     uint32_t *, FrameCounters *, int, cudaStream_t);
 int project_tile_size();
 void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const uint32_t *, int, int, const uint32_t *,
@@ -111,6 +112,7 @@ struct gsc_ctx {
   DevBuf<float2> spD;
   DevBuf<uint2> box;
   DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list, live_g;
+  DevBuf<uint32_t> live_bits;   // live bitset of the visible slots (live_mark -> live)
   DevBuf<uint32_t> pkey_b, pval_b;         // tile-sort scratch (front end only)
   DevBuf<uint32_t> sort_status_a, sort_status_b;
   size_t zero_bytes = 0, off_cull = 0, off_proj = 0, off_emit = 0;
@@ -321,6 +323,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->count.alloc(ctx->cap_splat));
   CU(ctx->gslot.alloc(ctx->cap_splat));
   CU(ctx->live_g.alloc(ctx->cap_splat / 2));
+  CU(ctx->live_bits.alloc(ctx->cap_splat / 64 + 1));
   CU(ctx->dkey_a.alloc(ctx->cap_splat));
   CU(ctx->dval_a.alloc(ctx->cap_splat));
   CU(ctx->dkey_b.alloc(ctx->cap_splat));
@@ -478,7 +481,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   // a4
   SplatBufs sb{S.spA.p, S.spB.p, S.spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
                ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
-  launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, ctx->live_g.p, sb,
+  launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, ctx->live_g.p, ctx->live_bits.p, sb,
                  reinterpret_cast<uint32_t *>(S.zero_region.p + ctx->off_proj), ctr, ctx->num_sms, sA);
   mark(sA);
   // a5 (depth digits of the (tile, depth) sort)

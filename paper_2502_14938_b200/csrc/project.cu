@@ -4,10 +4,10 @@
 // tile-coverage count (FlashGS citation), both eyes batched
 // ("independently or in batching"; R19).
 //
-// Two kernels.  live_kernel compacts the LIVE visible slots s = v*K + j
-// (255 alpha > 1; Gaussian g = X_f[v]*K + j) into live_g, in s order (hence
-// ascending g), with a CTA-level decoupled look-back over 4096-slot tiles: it
-// only reads 4 bytes per slot, so its look-back chain is short.
+// Three kernels.  live_mark_kernel + live_kernel compact the LIVE visible
+// slots s = v*K + j (255 alpha > 1; Gaussian g = X_f[v]*K + j) into live_g,
+// in s order (hence ascending g), as reduce-then-scan over 4096-slot tiles
+// (a live bitset and per-tile counts, then the expansion at each tile's prefix).
 // project_kernel then projects live item i for eye e in lane (i, e) -- every
 // lane busy -- walks the kept tiles of the warp's 32 splats (exact row-form
 // tile test, N7) into the kept-tile list with each pair's blend-block mask,
@@ -98,56 +98,91 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   return true;
 }
 
+// Pass 1 (independent tiles of 4096 slots): live bitset of the visible slots + per-tile live counts.
 __global__ void __launch_bounds__(kLThreads)
-live_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alpha, uint32_t *__restrict__ live_g,
-            uint32_t *__restrict__ status, FrameCounters *__restrict__ ctr) {
-  __shared__ uint32_t s_cnt[kLThreads / 32], s_red[kLThreads / 32 + 1], s_tile;
-  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
+live_mark_kernel(const uint32_t *__restrict__ visible, const float *__restrict__ alpha,
+                 uint32_t *__restrict__ live_bits, uint32_t *__restrict__ agg, const FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_cnt[kLThreads / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t S = ctr->n_visible * (uint32_t)kK;
   const uint32_t ntiles = (S + kLTile - 1) / kLTile;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = atomicAdd(&ctr->tile_project, 1u);
-    __syncthreads();
-    const uint32_t tile = s_tile;
-    if (tile >= ntiles) break;
-    uint32_t g[kLRounds], m[kLRounds], cnt = 0;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t s0 = tile * kLTile + warp * (32 * kLRounds) + lane;
+    float al[kLRounds];
 #pragma unroll
-    for (int r = 0; r < kLRounds; ++r) {
+    for (int r = 0; r < kLRounds; ++r) {   // all of the thread's loads in flight before the ballots
       const uint32_t s = s0 + 32 * r;
-      float al = 0.0f;
-      g[r] = 0;
+      al[r] = 0.0f;
       if (s < S) {
         const uint32_t v = s / kK, j = s - v * kK;
-        g[r] = visible[v] * kK + j;
-        al = alpha[g[r]];
+        al[r] = alpha[visible[v] * kK + j];
       }
-      m[r] = __ballot_sync(0xFFFFFFFFu, __fmul_rn(255.0f, al) > 1.0f);
-      cnt += __popc(m[r]);
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int r = 0; r < kLRounds; ++r) {
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, __fmul_rn(255.0f, al[r]) > 1.0f);
+      const uint32_t w = (s0 - lane) / 32 + r;
+      if (lane == 0 && 32 * w < S) live_bits[w] = m;
+      cnt += __popc(m);
     }
     if (lane == 0) s_cnt[warp] = cnt;
     __syncthreads();
-    uint32_t wex = 0, agg = 0;
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int w = 0; w < kLThreads / 32; ++w) t += s_cnt[w];
+      agg[tile] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// Pass 2: ordered compaction of the live slots s (hence ascending g) from the bitset at each tile's
+// prefix (sum of the earlier tiles' counts, L2-resident); the last tile sets n_splat = 2 x live.
+// (A single pass with a CTA-wide decoupled look-back spent most of its stall samples in the look-back.)
+__global__ void __launch_bounds__(kLThreads)
+live_kernel(const uint32_t *__restrict__ visible, const uint32_t *__restrict__ live_bits,
+            const uint32_t *__restrict__ agg, uint32_t *__restrict__ live_g, FrameCounters *__restrict__ ctr) {
+  __shared__ uint32_t s_pre[kLThreads / 32], s_cnt[kLThreads / 32];
+  const uint32_t warp = threadIdx.x >> 5, lane = lane_id(), lt = lanemask_lt();
+  const uint32_t S = ctr->n_visible * (uint32_t)kK;
+  const uint32_t ntiles = (S + kLTile - 1) / kLTile;
+  for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t pre = 0;
+    for (uint32_t j = threadIdx.x; j < tile; j += kLThreads) pre += agg[j];
+    pre = __reduce_add_sync(0xFFFFFFFFu, pre);
+    // warp w: words [16 w, 16 w + 16) of the tile (lane r < 16 holds word r)
+    const uint32_t w0 = tile * (kLTile / 32) + warp * kLRounds;
+    const uint32_t m = (lane < (uint32_t)kLRounds && 32 * (w0 + lane) < S) ? live_bits[w0 + lane] : 0u;
+    const uint32_t c = __popc(m);
+    uint32_t inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, inc, o);
+      if (lane >= (uint32_t)o) inc += t;
+    }
+    if (lane == 31) s_cnt[warp] = inc;
+    if (lane == 0) s_pre[warp] = pre;
+    __syncthreads();
+    uint32_t tpre = 0, wex = 0, tot = 0;
 #pragma unroll
     for (int w = 0; w < kLThreads / 32; ++w) {
-      const uint32_t c = s_cnt[w];
-      wex += (uint32_t)w < warp ? c : 0u;
-      agg += c;
+      tpre += s_pre[w];
+      wex += (uint32_t)w < warp ? s_cnt[w] : 0u;
+      tot += s_cnt[w];
     }
-    if (threadIdx.x == 0) st_volatile_u32(status + tile, (tile == 0 ? 2u << 30 : 1u << 30) | agg);
-    uint32_t pre = 0;
-    if (tile > 0) {
-      pre = block_lookback_u32<kLThreads>(status, tile, s_red);
-      if (threadIdx.x == 0) st_volatile_u32(status + tile, (2u << 30) | (pre + agg));
-    }
-    if (threadIdx.x == 0 && tile == ntiles - 1) ctr->n_splat = 2 * (pre + agg);
-    uint32_t base = pre + wex;
+    if (threadIdx.x == 0 && tile == ntiles - 1) ctr->n_splat = 2 * (tpre + tot);
+    const uint32_t ex = tpre + wex + inc - c;   // this lane's word's first output position
 #pragma unroll
     for (int r = 0; r < kLRounds; ++r) {
-      if ((m[r] >> lane) & 1u) live_g[base + __popc(m[r] & lt)] = g[r];
-      base += __popc(m[r]);
+      const uint32_t mr = __shfl_sync(0xFFFFFFFFu, m, r), br = __shfl_sync(0xFFFFFFFFu, ex, r);
+      if ((mr >> lane) & 1u) {
+        const uint32_t s = 32 * (w0 + r) + lane, v = s / kK, j = s - v * kK;
+        live_g[br + __popc(mr & lt)] = visible[v] * kK + j;
+      }
     }
-    __syncthreads();   // s_cnt / s_tile reuse
+    __syncthreads();   // s_pre / s_cnt reuse
   }
 }
 
@@ -467,8 +502,8 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
 static int g_live_grid = 0, g_project_grid = 0;
 
 void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
-                    uint32_t *live_g, const SplatBufs &sb, uint32_t *status, FrameCounters *ctr, int num_sms,
-                    cudaStream_t st) {
+                    uint32_t *live_g, uint32_t *live_bits, const SplatBufs &sb, uint32_t *status,
+                    FrameCounters *ctr, int num_sms, cudaStream_t st) {
   if (g_project_grid == 0) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, live_kernel, kLThreads, 0);
@@ -476,7 +511,8 @@ void launch_project(const FrameC &fc, const uint32_t *visible, const float *alph
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel<0>, kPThreads, 0);
     g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
   }
-  live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_g, status, ctr);
+  live_mark_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_bits, status, ctr);
+  live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, live_bits, status, live_g, ctr);
   switch (fc.ablate) {
 #define GSC_PROJ_CASE(k) \
   case k: project_kernel<k><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
