@@ -9,7 +9,7 @@ python bench.py --steps 600 --warmup 5 --no-cpu-baseline --stagger > gpurun_out/
 python bench.py --config C5 --steps 600 --warmup 5 --no-cpu-baseline > gpurun_out/prof2/bench_C5.txt 2>&1
 GSC_BENCH_SHARE_GPU=1 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 --steps 300 --warmup 5 --no-cpu-baseline > gpurun_out/prof2/bench_2rank.txt 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/prof2/launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline > gpurun_out/prof2/ncu_launch_run.txt 2>&1
-ncu --set full --clock-control none --import-source on -s 1600 -c 16 -o gpurun_out/prof2/frame100 python bench.py --steps 110 --warmup 3 --no-cpu-baseline > gpurun_out/prof2/ncu_full_run.txt 2>&1
+ncu --set full --clock-control none --import-source on -s 1700 -c 17 -o gpurun_out/prof2/frame100 python bench.py --steps 110 --warmup 3 --no-cpu-baseline > gpurun_out/prof2/ncu_full_run.txt 2>&1
 { echo "## memcheck"; timeout 900 compute-sanitizer --tool memcheck python -m pytest tests/test_gpu_parity.py -q -k "c1_all or reset or rgba8 or c1_abl or dered or host_async or c1_guide or stagger" 2>&1 | tail -4;
   echo "## racecheck"; timeout 600 compute-sanitizer --tool racecheck python -m pytest tests/test_gpu_parity.py -q -k "c1_all or stagger" 2>&1 | tail -3;
   echo "## synccheck"; timeout 600 compute-sanitizer --tool synccheck python -m pytest tests/test_gpu_parity.py -q -k "c1_all or stagger" 2>&1 | tail -3; } > gpurun_out/prof2/sanitizer.txt 2>&1
