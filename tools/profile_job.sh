@@ -16,5 +16,5 @@ timeout 800 python tools/cull_scale.py 18000000 60 gpurun_out/prof/cull_18M.json
   echo "## synccheck"; timeout 600 compute-sanitizer --tool synccheck python -m pytest tests/test_gpu_parity.py -q -k "c1_all or stagger" 2>&1 | tail -3; } > gpurun_out/prof/sanitizer.txt 2>&1
 PYTHONPATH=. timeout 300 python tools/elastic_session.py C4 15 72 120 2 gpurun_out/prof/elastic_C4.json > gpurun_out/prof/elastic.txt 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 800 --csv --log-file gpurun_out/prof/launches.csv python bench.py --steps 40 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_launch_run.txt 2>&1
-# one mid-trajectory frame: warm-up 3 frames + 97 timed = frame ~100 of the trajectory, 16 launches per frame
-ncu --set full --clock-control none --import-source on -s 1600 -c 16 -o gpurun_out/prof/frame100 python bench.py --steps 110 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_full_run.txt 2>&1
+# one mid-trajectory frame: warm-up 3 frames + 97 timed = frame ~100 of the trajectory, 17 launches per frame
+ncu --set full --clock-control none --import-source on -s 1700 -c 17 -o gpurun_out/prof/frame100 python bench.py --steps 110 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_full_run.txt 2>&1
