@@ -17,7 +17,12 @@ Parity status per function:
   derive                        pinned (fp64 numpy MLP, zero weights, Sigma
                                 closed forms / det / symmetry, mu formula)
   project / extent / tiles      pinned (on-axis closed form, r(alpha) closed
-                                forms, brute-force per-pixel tile sets)
+                                forms, brute-force per-pixel tile sets; off-axis:
+                                fp64 pinhole centres, finite-difference EWA
+                                Jacobian inside/outside the clamp, fp64 single-
+                                splat footprint, row-form kept set vs fp64 q_min
+                                on every splat of C1/C3 frames --
+                                tests/test_oracle_offaxis.py)
   sort                          pinned (numpy lexsort of the same pairs)
   blend                         pinned (empty, single splat, 13-splat stack,
                                 T monotone, weight sum <= 1, O2 == O1)
