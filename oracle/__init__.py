@@ -26,6 +26,10 @@ Parity status per function:
   sort                          pinned (numpy lexsort of the same pairs)
   blend                         pinned (empty, single splat, 13-splat stack,
                                 T monotone, weight sum <= 1, O2 == O1)
+  derive, real weights (F4)     pinned (fixed-order fp32 MLP: bit-exact against
+                                the exact rational on grid-valued inputs, within
+                                a derived bound of fp64 on real weights; epilogue
+                                shared with the grid path)
   depth-schedule shape H        parity unpinned beyond "linear"
 """
 from __future__ import annotations
@@ -62,7 +66,10 @@ class Scene(C.Structure):
                 ("pos", C.c_void_p), ("feat", C.c_void_p), ("offs", C.c_void_p),
                 ("scale", C.c_void_p), ("level", C.c_void_p),
                 ("W1", C.c_void_p), ("b1", C.c_void_p), ("W2a", C.c_void_p), ("b2a", C.c_void_p),
-                ("W2c", C.c_void_p), ("b2c", C.c_void_p), ("W2s", C.c_void_p), ("b2s", C.c_void_p)]
+                ("W2c", C.c_void_p), ("b2c", C.c_void_p), ("W2s", C.c_void_p), ("b2s", C.c_void_p),
+                ("real", C.c_int), ("featf", C.c_void_p), ("W1f", C.c_void_p), ("b1f", C.c_void_p),
+                ("W2af", C.c_void_p), ("b2af", C.c_void_p), ("W2cf", C.c_void_p), ("b2cf", C.c_void_p),
+                ("W2sf", C.c_void_p), ("b2sf", C.c_void_p)]
 
 
 class Config(C.Structure):
@@ -99,7 +106,8 @@ class Splat(C.Structure):
 class FrameStats(C.Structure):
     _fields_ = [("frame", C.c_int64), ("n_visible", C.c_int), ("n_hits", C.c_int), ("n_misses", C.c_int),
                 ("n_new", C.c_int), ("n_live", C.c_int), ("depth_used", C.c_int), ("depth_next", C.c_int),
-                ("n_splats", C.c_int64 * 2), ("n_pairs", C.c_int64 * 2), ("n_evals", C.c_int64)]
+                ("n_splats", C.c_int64 * 2), ("n_pairs", C.c_int64 * 2), ("n_evals", C.c_int64),
+                ("n_nonfinite", C.c_int64)]
 
 
 _lib = None
@@ -123,6 +131,8 @@ def lib():
         L.orc_build_cov.argtypes = [vp, vp, vp]
         L.orc_build_cov.restype = None
         L.orc_derive_anchor.argtypes = [C.POINTER(Scene), i32, vp, vp, vp, vp, vp, vp]
+        L.orc_mlp_f32.argtypes = [C.POINTER(Scene), vp, vp]
+        L.orc_mlp_f32.restype = None
         L.orc_derive_anchor.restype = None
         L.orc_project.argtypes = [C.POINTER(Config), C.POINTER(EyeConsts), f32, vp, vp, vp, C.POINTER(Splat)]
         L.orc_tile_kept.argtypes = [C.POINTER(Config), C.POINTER(Splat), i32, i32]
@@ -219,12 +229,17 @@ class SceneHolder:
         self.arrays = {}
         s = Scene()
         s.N, s.L, s.d0 = sc.n, sc.L, sc.d0
-        for name, dt in (("pos", np.float32), ("feat", np.int8), ("offs", np.float32), ("scale", np.float32),
-                         ("level", np.uint8), ("W1", np.int8), ("b1", np.int8), ("W2a", np.int8), ("b2a", np.int8),
-                         ("W2c", np.int8), ("b2c", np.int8), ("W2s", np.int8), ("b2s", np.int8)):
+        for name, dt in (("pos", np.float32), ("offs", np.float32), ("scale", np.float32), ("level", np.uint8)):
             a = np.ascontiguousarray(getattr(sc, name), dtype=dt)
             self.arrays[name] = a
             setattr(s, name, a.ctypes.data)
+        real = bool(getattr(sc, "real", False))
+        s.real = int(real)
+        # grid scenes: int8 codes in feat, W1, ...; real-weights scenes (F4): fp32 values in featf, W1f, ...
+        for name in ("feat", "W1", "b1", "W2a", "b2a", "W2c", "b2c", "W2s", "b2s"):
+            a = np.ascontiguousarray(getattr(sc, name), dtype=np.float32 if real else np.int8)
+            self.arrays[name] = a
+            setattr(s, name + "f" if real else name, a.ctypes.data)
         self.s = s
 
 
@@ -239,13 +254,21 @@ def derive_anchor(sh: SceneHolder, i: int, pu):
     return alpha, mu, cov, rgb, o
 
 
+def mlp_f32(sh: SceneHolder, x) -> np.ndarray:
+    """The real-weights path's fixed-order fp32 MLP (F4): x[35] -> o[110]."""
+    x = np.ascontiguousarray(np.asarray(x, np.float32))
+    o = np.zeros(NOUT, np.float32)
+    lib().orc_mlp_f32(C.byref(sh.s), _p(x), _p(o))
+    return o
+
+
 def project(cfg: Config, ec: EyeConsts, alpha, mu, cov, rgb):
     s = Splat()
     mu = np.asarray(mu, np.float32)
     cov = np.asarray(cov, np.float32)
     rgb = np.asarray(rgb, np.float32)
     ok = lib().orc_project(C.byref(cfg), C.byref(ec), float(alpha), _p(mu), _p(cov), _p(rgb), C.byref(s))
-    return (s if ok else None)
+    return (s if ok > 0 else None)
 
 
 @dataclass

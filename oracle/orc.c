@@ -302,41 +302,77 @@ void orc_build_cov(const float qin[4], const float S[3], float cov[6]) {
 /* ======================================================================
  * O-4 derivation (Eq. 3) with the exact-grid MLP (R3/R6).
  * ====================================================================== */
+/* F4 real-weights path: MLP_theta(f_i, d_view) of Eq. 3 with trained-style
+ * fp32 weights -- the three heads of reading R3, each Linear(35->32)-ReLU-Linear(32->n), evaluated in
+ * fp32 in a fixed order (F4): every output starts from its bias and accumulates its inputs
+ * in ascending index order, one fused multiply-add (fmaf, one rounding) per term:
+ *   h_c = max(0, fma(W1[34][c], x[34], ... fma(W1[0][c], x[0], b1[c])))
+ *   o_m = fma(W2[31][m], h[31], ... fma(W2[0][m], h[0], b2[m]))   (h of the head of output m) */
+void orc_mlp_f32(const orc_scene *sc, const float x[F + 3], float o[ORC_NOUT]) {
+  float a[3 * H];
+  for (int c = 0; c < 3 * H; ++c) {
+    float acc = sc->b1f[c];
+    for (int k = 0; k < F + 3; ++k) acc = fmaf(sc->W1f[k * 3 * H + c], x[k], acc);
+    a[c] = acc > 0.0f ? acc : 0.0f;            /* ReLU */
+  }
+  const float *W2[3] = {sc->W2af, sc->W2cf, sc->W2sf};
+  const float *b2[3] = {sc->b2af, sc->b2cf, sc->b2sf};
+  const int nh[3] = {K, 3 * K, 7 * K};
+  int base = 0;
+  for (int h = 0; h < 3; ++h) {
+    for (int m = 0; m < nh[h]; ++m) {
+      float acc = b2[h][m];
+      for (int u = 0; u < H; ++u) acc = fmaf(W2[h][u * nh[h] + m], a[h * H + u], acc);
+      o[base + m] = acc;
+    }
+    base += nh[h];
+  }
+}
+
 void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alpha, float *mu,
                        float *cov, float *rgb, float *o_raw) {
   const float *p = sc->pos + 3 * (size_t)i;
   const float *s = sc->scale + 3 * (size_t)i;
   float v[3] = {p[0] - pu[0], p[1] - pu[1], p[2] - pu[2]};
   float n = sqrtf(dot3(v, v));
-  int x[F + 3];
-  for (int k = 0; k < F; ++k) x[k] = sc->feat[(size_t)i * F + k];
-  for (int k = 0; k < 3; ++k) {
-    float dv = (n == 0.0f) ? 0.0f : v[k] / n;
-    long q = lrintf(128.0f * dv);            /* round half to even */
-    if (q < -127) q = -127;
-    if (q > 127) q = 127;
-    x[F + k] = (int)q;
-  }
-  /* layer 1 (three heads side by side): z1 = W1 x + 128 b1  (value z1 / 2^14) */
-  int64_t a[3 * H];
-  for (int c = 0; c < 3 * H; ++c) {
-    int64_t acc = 128 * (int64_t)sc->b1[c];
-    for (int k = 0; k < F + 3; ++k) acc += (int64_t)sc->W1[k * 3 * H + c] * x[k];
-    a[c] = acc > 0 ? acc : 0;                  /* ReLU */
-  }
-  /* layer 2 per head: z2 = W2 a + 2^14 b2 (value z2 / 2^21); one RNE conversion */
   float o[ORC_NOUT];
-  const int8_t *W2[3] = {sc->W2a, sc->W2c, sc->W2s};
-  const int8_t *b2[3] = {sc->b2a, sc->b2c, sc->b2s};
-  const int nh[3] = {K, 3 * K, 7 * K};
-  int base = 0;
-  for (int h = 0; h < 3; ++h) {
-    for (int m = 0; m < nh[h]; ++m) {
-      int64_t acc = 16384 * (int64_t)b2[h][m];
-      for (int u = 0; u < H; ++u) acc += (int64_t)W2[h][u * nh[h] + m] * a[h * H + u];
-      o[base + m] = (float)acc * 4.76837158203125e-07f; /* 2^-21, exact */
+  if (sc->real) {
+    /* F4: continuous view direction d_view = v / |v| (three IEEE divisions; 0 at the camera) */
+    float xf[F + 3];
+    for (int k = 0; k < F; ++k) xf[k] = sc->featf[(size_t)i * F + k];
+    for (int k = 0; k < 3; ++k) xf[F + k] = (n == 0.0f) ? 0.0f : v[k] / n;
+    orc_mlp_f32(sc, xf, o);
+  } else {
+    /* grid path (R3/R6): quantised view direction, exact-integer MLP */
+    int x[F + 3];
+    for (int k = 0; k < F; ++k) x[k] = sc->feat[(size_t)i * F + k];
+    for (int k = 0; k < 3; ++k) {
+      float dv = (n == 0.0f) ? 0.0f : v[k] / n;
+      long q = lrintf(128.0f * dv);            /* round half to even */
+      if (q < -127) q = -127;
+      if (q > 127) q = 127;
+      x[F + k] = (int)q;
     }
-    base += nh[h];
+    /* layer 1 (three heads side by side): z1 = W1 x + 128 b1  (value z1 / 2^14) */
+    int64_t a[3 * H];
+    for (int c = 0; c < 3 * H; ++c) {
+      int64_t acc = 128 * (int64_t)sc->b1[c];
+      for (int k = 0; k < F + 3; ++k) acc += (int64_t)sc->W1[k * 3 * H + c] * x[k];
+      a[c] = acc > 0 ? acc : 0;                  /* ReLU */
+    }
+    /* layer 2 per head: z2 = W2 a + 2^14 b2 (value z2 / 2^21); one RNE conversion */
+    const int8_t *W2[3] = {sc->W2a, sc->W2c, sc->W2s};
+    const int8_t *b2[3] = {sc->b2a, sc->b2c, sc->b2s};
+    const int nh[3] = {K, 3 * K, 7 * K};
+    int base = 0;
+    for (int h = 0; h < 3; ++h) {
+      for (int m = 0; m < nh[h]; ++m) {
+        int64_t acc = 16384 * (int64_t)b2[h][m];
+        for (int u = 0; u < H; ++u) acc += (int64_t)W2[h][u * nh[h] + m] * a[h * H + u];
+        o[base + m] = (float)acc * 4.76837158203125e-07f; /* 2^-21, exact */
+      }
+      base += nh[h];
+    }
   }
   if (o_raw) memcpy(o_raw, o, sizeof(o));
   const float *oa = o, *oc = o + K, *os = o + 4 * K;
@@ -359,10 +395,17 @@ void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alp
 #define ORC_KAPPA 1.0009765625f   /* 1 + 2^-10 */
 #define ORC_SLACK 0.015625f       /* 2^-6 */
 
+/* Returns 1 (projected), 0 (culled) or -1: skipped for non-finite splat parameters ("non-finite
+ * splat parameters -> skip splat, count in FrameRecord diagnostics"): a non-finite mean or covariance
+ * entry, or, for a Gaussian inside the depth range, a non-finite determinant, conic or centre. */
 int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, const float *mu,
                 const float *cov, const float *rgb, orc_splat *o) {
   float rho = 255.0f * alpha;
   if (!(rho > 1.0f)) return 0;                              /* alpha <= eps => cull */
+  for (int k = 0; k < 3; ++k)
+    if (!isfinite(mu[k])) return -1;
+  for (int k = 0; k < 6; ++k)
+    if (!isfinite(cov[k])) return -1;
   float t[3] = {mu[0] - ec->p[0], mu[1] - ec->p[1], mu[2] - ec->p[2]};
   float x = dot3(t, ec->r0), y = dot3(t, ec->r1), z = dot3(t, ec->r2);
   if (!(z > ec->near_plane) || z > ec->far_plane) return 0;
@@ -388,6 +431,7 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
   a = a + 0.3f;                                             /* S:349, S:391 */
   c = c + 0.3f;
   float det = (a * c) - (b * b);
+  if (!isfinite(det)) return -1;
   if (!(det > 0.0f)) return 0;
   float idet = 1.0f / det;
   o->A = c * idet;
@@ -403,7 +447,7 @@ int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, co
   o->depth = z;
   if (!isfinite(o->A) || !isfinite(o->B) || !isfinite(o->C) || !isfinite(o->u) || !isfinite(o->v) ||
       !isfinite(o->thr))
-    return 0;
+    return -1;
   /* candidate box: ellipse AABB sqrt(thr * Sigma'_xx) (+1 px pad), clamped to the screen tiles */
   int TW = (cfg->width + 15) / 16, TH = (cfg->height + 15) / 16;
   float ex = sqrtf(o->thr * a) + 1.0f, ey = sqrtf(o->thr * c) + 1.0f;
@@ -697,14 +741,15 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
 #pragma omp parallel for schedule(dynamic, 256)
     for (int64_t s = 0; s < S; ++s) {
       int64_t g = (int64_t)st->visible[s / K] * K + (s % K);
-      ok[s] = (unsigned char)orc_project(cfg, &ec[e], st->alpha[g], st->mu + 3 * g, st->cov + 6 * g,
-                                          st->rgb + 3 * g, &tmp_spl[s]);
+      int r = orc_project(cfg, &ec[e], st->alpha[g], st->mu + 3 * g, st->cov + 6 * g, st->rgb + 3 * g, &tmp_spl[s]);
+      ok[s] = (unsigned char)(r > 0 ? 1 : r < 0 ? 2 : 0);
     }
-    int64_t n = 0, np = 0, nlive = 0;
+    int64_t n = 0, np = 0, nlive = 0, nnf = 0;
     for (int64_t s = 0; s < S; ++s) {
       int64_t g = (int64_t)st->visible[s / K] * K + (s % K);
       if (e == 0 && st->alpha[g] > 0.0f) ++nlive;
-      if (!ok[s]) continue;
+      if (ok[s] == 2) ++nnf;                                /* non-finite: skipped and counted */
+      if (ok[s] != 1) continue;
       st->spl[e][n] = tmp_spl[s];
       st->spl_g[e][n] = (uint32_t)g;
       np += tmp_spl[s].ntiles;
@@ -715,6 +760,7 @@ int orc_frame(orc_state *st, const orc_eye *l, const orc_eye *r, unsigned flags,
     total_pairs += np;
     if (stats) {
       stats->n_splats[e] = n; stats->n_pairs[e] = np;
+      stats->n_nonfinite += nnf;
       if (e == 0) stats->n_live = (int)nlive;
     }
   }

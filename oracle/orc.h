@@ -44,6 +44,11 @@ typedef struct {
   const float *scale;    /* [N*3] */
   const uint8_t *level;  /* [N] */
   const int8_t *W1, *b1, *W2a, *b2a, *W2c, *b2c, *W2s, *b2s;
+  /* real-weights path: real != 0 selects fp32 features and decoder
+   * weights (same shapes as the codes above, any values) and the unquantised view direction */
+  int real;
+  const float *featf;    /* [N*F] */
+  const float *W1f, *b1f, *W2af, *b2af, *W2cf, *b2cf, *W2sf, *b2sf;
 } orc_scene;
 
 typedef struct {
@@ -92,6 +97,7 @@ typedef struct {
   int n_visible, n_hits, n_misses, n_new, n_live, depth_used, depth_next;
   int64_t n_splats[2], n_pairs[2];
   int64_t n_evals; /* per-pixel splat evaluations in the blend */
+  int64_t n_nonfinite; /* (Gaussian, eye) pairs skipped for non-finite splat parameters */
 } orc_frame_stats;
 
 /* ---- elementary functions (DESIGN.md Numerics E1-E4) ---- */
@@ -110,8 +116,11 @@ float orc_margin(const float *offs_i, const float *s_i);
 int orc_lod_cut(const orc_unified *u, int L, float d0, const float *p);
 int orc_visible(const orc_unified *u, int L, float d0, const float *p, float margin, int level);
 void orc_build_cov(const float q[4], const float S[3], float cov[6]);
+/* F4: the fixed-order fp32 MLP of the real-weights path: x[35] (32 features, d_view) -> o[110] */
+void orc_mlp_f32(const orc_scene *sc, const float x[ORC_F + 3], float o[ORC_NOUT]);
 void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alpha, float *mu,
                        float *cov, float *rgb, float *o_raw /* [110] or NULL */);
+/* 1 projected, 0 culled, -1 skipped for non-finite parameters (counted) */
 int orc_project(const orc_config *cfg, const orc_eye_consts *ec, float alpha, const float *mu,
                 const float *cov, const float *rgb, orc_splat *out);
 int orc_tile_kept(const orc_config *cfg, const orc_splat *s, int tx, int ty);

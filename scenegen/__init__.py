@@ -36,7 +36,7 @@ import numpy as np
 
 __all__ = [
     "splitmix64", "uniform01", "Scene", "Rig", "make_city_scene",
-    "make_orbit", "look_at_rig", "write_gsc2", "read_gsc2",
+    "make_orbit", "look_at_rig", "write_gsc2", "read_gsc2", "with_real_weights",
     "write_trajectory", "read_trajectory", "config", "CONFIGS",
     "F_DIM", "K_GAUSS", "H_DIM",
 ]
@@ -97,6 +97,8 @@ class Scene:
     L: int
     d0: float
     bbox: np.ndarray = field(default_factory=lambda: np.zeros(6, np.float32))
+    # real-weights scene: feat and the decoder weights are fp32 values, not int8 codes
+    real: bool = False
 
     @property
     def n(self) -> int:
@@ -221,6 +223,24 @@ def make_city_scene(seed: int, n: int, side: float, L: int = 5, width: int = 192
                  L=L, d0=float(np.float32(d0)), bbox=bbox)
 
 
+def with_real_weights(scene: Scene, seed: int = 11) -> Scene:
+    """F4 input: the same anchors with trained-style fp32 features and decoder
+    weights -- continuous values, not on the 2^-7 grid.  Features U(-1, 1); each weight and bias
+    uniform in +-(the grid scene's Kaiming code bound)/128 (W1, b1: 21; W2a: 64; b2a and the colour /
+    covariance heads: 22), so activations and opacities spread like the grid scene's."""
+    import dataclasses
+    n, F, K, H = scene.n, F_DIM, K_GAUSS, H_DIM
+
+    def U(stream, shape, bound):
+        cnt = int(np.prod(shape))
+        return ((uniform01(seed, stream, cnt) * 2.0 - 1.0) * (bound / 128.0)).astype(np.float32).reshape(shape)
+
+    return dataclasses.replace(
+        scene, feat=U(30, (n, F), 128.0), W1=U(31, (F + 3, 3 * H), 21), b1=U(32, (3 * H,), 21),
+        W2a=U(33, (H, K), 64), b2a=U(34, (K,), 22), W2c=U(35, (H, 3 * K), 22), b2c=U(36, (3 * K,), 22),
+        W2s=U(37, (H, 7 * K), 22), b2s=U(38, (7 * K,), 22), real=True)
+
+
 # ----------------------------------------------------------------------------
 # cameras
 # ----------------------------------------------------------------------------
@@ -297,19 +317,21 @@ _HDR = struct.Struct("<4sIIIIIIf6f")  # magic, version, N, F, K, L, H, d0, bbox
 def write_gsc2(scene: Scene, path: str) -> None:
     """GSC2: GSC1 as SoA with int8 grid codes and the three-head weights.
 
-    header  : "GSC2" u32 version=2, u32 N, u32 F, u32 K, u32 L, u32 H, f32 d0, f32 bbox[6]
-    arrays  : pos f32[N*3] | feat i8[N*F] | offs f32[N*K*3] | scale f32[N*3] | level u8[N]
-    weights : W1 i8[(F+3)*3H] | b1 i8[3H] | W2a i8[H*K] | b2a i8[K] | W2c i8[H*3K] |
-              b2c i8[3K] | W2s i8[H*7K] | b2s i8[7K]
+    header  : "GSC2" u32 version, u32 N, u32 F, u32 K, u32 L, u32 H, f32 d0, f32 bbox[6]
+    arrays  : pos f32[N*3] | feat q[N*F] | offs f32[N*K*3] | scale f32[N*3] | level u8[N]
+    weights : W1 q[(F+3)*3H] | b1 q[3H] | W2a q[H*K] | b2a q[K] | W2c q[H*3K] |
+              b2c q[3K] | W2s q[H*7K] | b2s q[7K]
+    version 2: q = i8 grid codes (value = code / 128); version 3 (real-weights scenes, F4): q = f32.
     """
+    q = "<f4" if scene.real else "i1"
     with open(path, "wb") as fh:
-        fh.write(_HDR.pack(b"GSC2", 2, scene.n, F_DIM, K_GAUSS, scene.L, H_DIM,
+        fh.write(_HDR.pack(b"GSC2", 3 if scene.real else 2, scene.n, F_DIM, K_GAUSS, scene.L, H_DIM,
                            scene.d0, *[float(x) for x in scene.bbox]))
-        for a, dt in ((scene.pos, "<f4"), (scene.feat, "i1"), (scene.offs, "<f4"),
-                      (scene.scale, "<f4"), (scene.level, "u1"), (scene.W1, "i1"),
-                      (scene.b1, "i1"), (scene.W2a, "i1"), (scene.b2a, "i1"),
-                      (scene.W2c, "i1"), (scene.b2c, "i1"), (scene.W2s, "i1"),
-                      (scene.b2s, "i1")):
+        for a, dt in ((scene.pos, "<f4"), (scene.feat, q), (scene.offs, "<f4"),
+                      (scene.scale, "<f4"), (scene.level, "u1"), (scene.W1, q),
+                      (scene.b1, q), (scene.W2a, q), (scene.b2a, q),
+                      (scene.W2c, q), (scene.b2c, q), (scene.W2s, q),
+                      (scene.b2s, q)):
             fh.write(np.ascontiguousarray(a, dtype=dt).tobytes())
 
 
@@ -319,8 +341,9 @@ def read_gsc2(path: str) -> Scene:
     if len(data) < _HDR.size:
         raise ValueError(f"GSC2 truncated header at offset {len(data)}")
     magic, ver, n, F, K, L, H, d0, *bbox = _HDR.unpack_from(data, 0)
-    if magic != b"GSC2" or ver != 2:
+    if magic != b"GSC2" or ver not in (2, 3):
         raise ValueError("GSC2 bad magic/version at offset 0")
+    q = "<f4" if ver == 3 else "i1"
     off = _HDR.size
 
     def take(count, dt, shape):
@@ -333,20 +356,20 @@ def read_gsc2(path: str) -> Scene:
         return a
 
     pos = take(n * 3, "<f4", (n, 3))
-    feat = take(n * F, "i1", (n, F))
+    feat = take(n * F, q, (n, F))
     offs = take(n * K * 3, "<f4", (n, K, 3))
     scale = take(n * 3, "<f4", (n, 3))
     level = take(n, "u1", (n,))
-    W1 = take((F + 3) * 3 * H, "i1", (F + 3, 3 * H))
-    b1 = take(3 * H, "i1", (3 * H,))
-    W2a = take(H * K, "i1", (H, K))
-    b2a = take(K, "i1", (K,))
-    W2c = take(H * 3 * K, "i1", (H, 3 * K))
-    b2c = take(3 * K, "i1", (3 * K,))
-    W2s = take(H * 7 * K, "i1", (H, 7 * K))
-    b2s = take(7 * K, "i1", (7 * K,))
+    W1 = take((F + 3) * 3 * H, q, (F + 3, 3 * H))
+    b1 = take(3 * H, q, (3 * H,))
+    W2a = take(H * K, q, (H, K))
+    b2a = take(K, q, (K,))
+    W2c = take(H * 3 * K, q, (H, 3 * K))
+    b2c = take(3 * K, q, (3 * K,))
+    W2s = take(H * 7 * K, q, (H, 7 * K))
+    b2s = take(7 * K, q, (7 * K,))
     return Scene(pos=pos, feat=feat, offs=offs, scale=scale, level=level, W1=W1, b1=b1,
-                 W2a=W2a, b2a=b2a, W2c=W2c, b2c=b2c, W2s=W2s, b2s=b2s, L=L, d0=d0,
+                 W2a=W2a, b2a=b2a, W2c=W2c, b2c=b2c, W2s=W2s, b2s=b2s, L=L, d0=d0, real=ver == 3,
                  bbox=np.array(bbox, np.float32))
 
 
@@ -386,10 +409,11 @@ class Config:
     seed: int = 7
     near: float = 0.05
     far: float = 5000.0
+    real: bool = False     # F4: fp32 non-grid features / decoder weights (with_real_weights)
 
     def scene(self) -> Scene:
-        return make_city_scene(self.seed, self.n, self.side, self.L, self.width, self.height,
-                               self.fov_y_deg)
+        sc = make_city_scene(self.seed, self.n, self.side, self.L, self.width, self.height, self.fov_y_deg)
+        return with_real_weights(sc) if self.real else sc
 
     @property
     def center(self):
@@ -407,6 +431,11 @@ CONFIGS = {
     "C4": Config("C4", 1_000_000, 400.0, 5, 1920, 1080, 70.0, 10),
     # configs[4]: 5M city, 2K binocular, split across GPUs
     "C5": Config("C5", 5_000_000, 900.0, 5, 1920, 1080, 70.0, 10),
+    # SURVEY §8(f) F4 (real-weights path): the C1 / C3 scenes with fp32 non-grid features and decoder
+    # weights, and a Scaffold-GS-style scene (L = 1: no LoD) with real weights on the C3 orbit
+    "C1R": Config("C1R", 1000, 20.0, 3, 64, 64, 70.0, 10, real=True),
+    "C3R": Config("C3R", 100_000, 130.0, 5, 1920, 1080, 70.0, 10, real=True),
+    "C3S": Config("C3S", 100_000, 130.0, 1, 1920, 1080, 70.0, 10, real=True),
 }
 
 
@@ -431,18 +460,19 @@ def trajectory(cfg: Config, n_frames: int | None = None):
     """The trajectory of a config."""
     s = cfg.side
     c = cfg.center
-    if cfg.name == "C1":
+    name = cfg.name[:2]          # C1R / C3R / C3S follow their base config's trajectory
+    if name == "C1":
         return c1_poses(cfg)
-    if cfg.name == "C2":
+    if name == "C2":
         # two static poses, 100 frames each
         n = n_frames or 200
         a = look_at_rig(c + np.array([0.35 * s, 0.0, 1.7]), c, 0.064)
         b = look_at_rig(c + np.array([0.35 * s, 0.0, 60.0]), c, 0.064)
         return [a if f < n // 2 else b for f in range(n)]
-    if cfg.name == "C3":
+    if name == "C3":
         return make_orbit(c, 0.35 * s, 0.35 * s, 1.7, 60.0, n_frames or 300, 0.3)
-    if cfg.name == "C4":
+    if name == "C4":
         return make_orbit(c, 0.3 * s, 0.7 * s, 1.7, 300.0, n_frames or 600, 0.25)
-    if cfg.name == "C5":
+    if name == "C5":
         return make_orbit(c, 0.3 * s, 0.7 * s, 1.7, 300.0, n_frames or 2400, 0.25)
     raise KeyError(cfg.name)
