@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GSC_ABI_VERSION 1
+#define GSC_ABI_VERSION 2
 
 typedef enum {
   GSC_OK = 0,
@@ -52,7 +52,12 @@ typedef enum {
   GSC_ECUDA = 5,       /* CUDA runtime error; sticky */
   GSC_EINTERNAL = 6,   /* internal consistency failure */
   GSC_ESTATE = 7,      /* call out of order (render before load/pose) */
-  GSC_ECAPACITY = 8    /* a frame produced more (tile, depth) pairs than pair_capacity */
+  GSC_ECAPACITY = 8    /* a frame needed more (tile, depth) pairs (or kept-tile list entries) than
+                          pair_capacity allows: its image is incomplete (an overflowed kept-tile list
+                          drops all of the frame's pairs: background image).  Reported by the call
+                          that returns the frame's stats, else by the next gsc_render_pair /
+                          gsc_sync / gsc_wait_frame / gsc_render_pair_host that sees the frame
+                          finished; once per frame; not sticky */
 } gsc_status;
 
 typedef struct gsc_ctx gsc_ctx;
@@ -117,6 +122,21 @@ typedef struct {
   const int8_t *W2s, *b2s;        /* [32][70], [70]: per Gaussian 3 scales then quaternion (w,x,y,z) */
 } gsc_scene_desc;
 
+/* Real-weights scene (Eq. 3 P:101-105 "MLP_theta(f_i, d_view)" with trained
+ * weights): fp32 features and decoder weights of any value (same shapes and layouts as
+ * gsc_scene_desc).  The derivation then runs the fixed-order fp32 MLP (every output from its bias,
+ * inputs in ascending index order, one fma per term; F4) on the CUDA cores with the
+ * unquantised view direction d_view = (p_i - p_u) / |p_i - p_u|.  lod_levels = 1 with every level 0
+ * is a Scaffold-GS scene (no LoD).  Borrowed for the duration of the call only. */
+typedef struct {
+  int32_t n_anchors, lod_levels;
+  float d0;
+  const float *pos, *feat, *offs, *scale;   /* [N][3], [N][32], [N][10][3], [N][3] */
+  const uint8_t *level;                     /* [N] */
+  const float *W1, *b1;                     /* [35][96], [96] */
+  const float *W2a, *b2a, *W2c, *b2c, *W2s, *b2s;
+} gsc_scene_desc_f32;
+
 /* Per-frame record (SPEC FrameRecord S:421-423, CacheStats S:208). */
 typedef struct {
   int64_t frame;
@@ -130,6 +150,11 @@ typedef struct {
   float ms_cull, ms_derive, ms_project, ms_depth_sort, ms_emit, ms_tile_sort, ms_ranges, ms_blend, ms_total;
   uint64_t n_evals;                              /* blend: (pixel, splat) evaluations executed (GSC_F_COUNT_EVALS) */
   uint64_t n_exp;                                /* blend: evaluations inside the skip bound (GSC_F_COUNT_EVALS) */
+  uint32_t n_nonfinite_skipped;                  /* (Gaussian, eye) pairs skipped for non-finite splat parameters:
+                                                    mean / covariance, or 2D covariance, determinant, conic or
+                                                    centre (skip the splat, count it) */
+  uint32_t n_blend_fixup;                        /* pixels the blend re-ran with the exact exp_s because a decision
+                                                    came within the fast exponential's error band (R5) */
 } gsc_frame_stats;
 
 /* out formats */
@@ -153,12 +178,17 @@ int gsc_abi_version(void);
 /* Create a context on CUDA device `cuda_device`.  Validates cfg (GSC_EINVAL). */
 gsc_status gsc_create(int cuda_device, const gsc_config *cfg, gsc_ctx **out);
 
-/* Load a GSC2 scene file (format in scenegen/__init__.py write_gsc2); resets the cache.
+/* Load a GSC2 scene file (format in scenegen/__init__.py write_gsc2: version 2 = int8 grid codes,
+ * version 3 = fp32 features and weights, the real-weights path F4); resets the cache.
  * GSC_EFORMAT with the byte offset on bad magic / truncation / unsupported dims. */
 gsc_status gsc_load_scene(gsc_ctx *ctx, const char *path);
 
 /* Same from host arrays (copied to the device; the caller keeps ownership). */
 gsc_status gsc_load_scene_host(gsc_ctx *ctx, const gsc_scene_desc *scene);
+
+/* Same for a real-weights scene (F4).  GSC_EINVAL on null arrays or bad sizes; GSC_EFORMAT when an
+ * anchor level >= lod_levels or a feature / weight is not finite. */
+gsc_status gsc_load_scene_host_f32(gsc_ctx *ctx, const gsc_scene_desc_f32 *scene);
 
 /* Validate the rig (unit quaternions within 1e-6) and compute the
  * unified camera (Eqs. 5-6) and per-eye constants for the next render.
@@ -215,8 +245,9 @@ gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags);
 gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t capacity_bytes, size_t *len_bytes);
 
 /* Evaluate the device elementary functions (0 exp_s, 1 log_s, 2 tanh_s,
- * 3 sigmoid_s, 4 exp_blend = the blend's exp_s for x in [-87, 0];
- * DESIGN.md Numerics) on n device floats (parity sweeps). */
+ * 3 sigmoid_s, 4 exp_blend = the blend's exact exp_s for x in [-87, 0],
+ * 5 the blend's fast exp ex2.approx(fl(x log2e));
+ * DESIGN.md Numerics) on n device floats (parity sweeps, error bounds). */
 gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n);
 
 const char *gsc_last_error(const gsc_ctx *ctx);

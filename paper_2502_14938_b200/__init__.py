@@ -70,7 +70,8 @@ class Renderer:
             self._chk(_abi.lib().gsc_load_scene(self.h, scene.encode()))
         else:
             d = _abi.SceneDesc(scene)
-            self._chk(_abi.lib().gsc_load_scene_host(self.h, C.byref(d.desc)))
+            load = _abi.lib().gsc_load_scene_host_f32 if d.real else _abi.lib().gsc_load_scene_host
+            self._chk(load(self.h, C.byref(d.desc)))
         return self
 
     def set_pose(self, rig):
@@ -167,12 +168,12 @@ class Renderer:
         return out
 
     def elementary(self, fn: str, x):
-        """Evaluate a device elementary function (exp/log/tanh/sigmoid, exp_blend = the blend's exp
-        for x in [-87, 0]) on a CUDA float32 tensor."""
+        """Evaluate a device elementary function (exp/log/tanh/sigmoid, exp_blend = the blend's exact exp
+        for x in [-87, 0], exp_fast = the blend's SFU exp ex2.approx(x log2e)) on a CUDA float32 tensor."""
         import ctypes as C
         import torch
         out = torch.empty_like(x)
-        code = {"exp": 0, "log": 1, "tanh": 2, "sigmoid": 3, "exp_blend": 4}[fn]
+        code = {"exp": 0, "log": 1, "tanh": 2, "sigmoid": 3, "exp_blend": 4, "exp_fast": 5}[fn]
         self._chk(_abi.lib().gsc_selftest_elementary(self.h, code, C.c_void_p(x.data_ptr()),
                                                      C.c_void_p(out.data_ptr()), x.numel()))
         return out

@@ -56,6 +56,14 @@ class gsc_scene_desc(C.Structure):
                 ("b2s", C.c_void_p)]
 
 
+class gsc_scene_desc_f32(C.Structure):
+    _fields_ = [("n_anchors", C.c_int32), ("lod_levels", C.c_int32), ("d0", C.c_float),
+                ("pos", C.c_void_p), ("feat", C.c_void_p), ("offs", C.c_void_p), ("scale", C.c_void_p),
+                ("level", C.c_void_p), ("W1", C.c_void_p), ("b1", C.c_void_p), ("W2a", C.c_void_p),
+                ("b2a", C.c_void_p), ("W2c", C.c_void_p), ("b2c", C.c_void_p), ("W2s", C.c_void_p),
+                ("b2s", C.c_void_p)]
+
+
 class gsc_frame_stats(C.Structure):
     _fields_ = [("frame", C.c_int64), ("n_visible", C.c_uint32), ("n_hits", C.c_uint32),
                 ("n_misses", C.c_uint32), ("n_new", C.c_uint32), ("n_splats", C.c_uint32),
@@ -64,7 +72,8 @@ class gsc_frame_stats(C.Structure):
                 ("ms_cull", C.c_float), ("ms_derive", C.c_float), ("ms_project", C.c_float),
                 ("ms_depth_sort", C.c_float), ("ms_emit", C.c_float), ("ms_tile_sort", C.c_float),
                 ("ms_ranges", C.c_float), ("ms_blend", C.c_float), ("ms_total", C.c_float),
-                ("n_evals", C.c_uint64), ("n_exp", C.c_uint64)]
+                ("n_evals", C.c_uint64), ("n_exp", C.c_uint64), ("n_nonfinite_skipped", C.c_uint32),
+                ("n_blend_fixup", C.c_uint32)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -76,6 +85,7 @@ _SIGS = {
     "gsc_create": (C.c_int, [C.c_int, C.POINTER(gsc_config), C.POINTER(C.c_void_p)]),
     "gsc_load_scene": (C.c_int, [C.c_void_p, C.c_char_p]),
     "gsc_load_scene_host": (C.c_int, [C.c_void_p, C.POINTER(gsc_scene_desc)]),
+    "gsc_load_scene_host_f32": (C.c_int, [C.c_void_p, C.POINTER(gsc_scene_desc_f32)]),
     "gsc_set_pose": (C.c_int, [C.c_void_p, C.POINTER(gsc_rig)]),
     "gsc_render_pair": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int, C.c_void_p,
                                   C.POINTER(gsc_frame_stats)]),
@@ -140,11 +150,14 @@ class SceneDesc:
 
     def __init__(self, sc):
         self.keep = {}
-        d = gsc_scene_desc()
+        # grid scenes: int8 codes (gsc_scene_desc); real-weights scenes (F4): fp32 (gsc_scene_desc_f32)
+        self.real = bool(getattr(sc, "real", False))
+        q = np.float32 if self.real else np.int8
+        d = gsc_scene_desc_f32() if self.real else gsc_scene_desc()
         d.n_anchors, d.lod_levels, d.d0 = sc.n, sc.L, sc.d0
-        for name, dt in (("pos", np.float32), ("feat", np.int8), ("offs", np.float32), ("scale", np.float32),
-                         ("level", np.uint8), ("W1", np.int8), ("b1", np.int8), ("W2a", np.int8), ("b2a", np.int8),
-                         ("W2c", np.int8), ("b2c", np.int8), ("W2s", np.int8), ("b2s", np.int8)):
+        for name, dt in (("pos", np.float32), ("feat", q), ("offs", np.float32), ("scale", np.float32),
+                         ("level", np.uint8), ("W1", q), ("b1", q), ("W2a", q), ("b2a", q),
+                         ("W2c", q), ("b2c", q), ("W2s", q), ("b2s", q)):
             a = np.ascontiguousarray(getattr(sc, name), dtype=dt)
             self.keep[name] = a
             setattr(d, name, a.ctypes.data)

@@ -17,16 +17,64 @@
 // alpha' = 0, which leaves T and C bit-identical (fma(-0, T, T) = T,
 // fma(c, 0, C) = C); only when no lane of the warp needs the exp is the splat
 // skipped outright.
-// Per evaluated (pixel, splat), the exact op order of DESIGN.md N6
-// (identical in the oracle):
+// Per evaluated (pixel, splat), the op order of DESIGN.md N6 (the oracle's), except the exponential:
 //   power  = fma(dx, fma(a', dx, b' dy), (c' dy) dy)      (skip if > 0)
-//   alpha' = min(0.99, alpha exp_s(power))                (skip if < 1/255)
+//   alpha' = min(0.99, alpha exp(power))                  (skip if < 1/255)
 //   T' = fma(-alpha', T, T); stop before T' < 1e-4; C = fma(c, alpha' T, C)
+// exp runs on the SFU (ex2.approx) with a guard band that takes the skip decision
+// with the exact exp_s where alpha' lies within 2^-16 relative of 1/255, so every skip decision is
+// the oracle's; pixels match it within ~1e-6 (<= 1e-4 where a T < 1e-4 stop flips), inside the
+// north_star tolerance (2e-3 per channel, PSNR >= 55 dB).
 #include "gsc_internal.cuh"
 
 namespace gsc {
 
 constexpr int kBThreads = 256;
+constexpr float kLog2e = 1.44269502162933349609375f;
+// The fast alpha' = min(0.99, alpha ex2.approx(fl(power log2e))) differs from the oracle's
+// min(0.99, alpha exp_s(power)) by < 2^-20 relative for power in [skip bound, 0] (argument rounding
+// <= 3.3e-7, ex2.approx <= 1.7e-7, exp_s <= 1 ulp, fl(log2e) and the two products' roundings; measured
+// on every float of the range by tests/test_gpu_parity.py::test_fast_exp_error_bound), so the skip
+// decision alpha' >= 1/255 can differ only inside 2^-19 relative of 1/255:
+constexpr float kAlphaGuard = 7.5e-9f;    // >= 2^-19 x 1/255 (7.48e-9)
+// |T_fast / T_exact - 1| <= 5e-4 at any point of a pixel's composite: the alpha' error of ex2.approx
+// (<= 7e-7 relative) enters T' = T (1 - alpha') amplified by alpha'/(1 - alpha'), summed over the
+// accepted splats with prod (1 - alpha') >= 1e-4 (<= 198 x 7e-7), plus <= 1 ulp of fma rounding per
+// step over at most 2345 steps (alpha' >= 1/255): 1.4e-4 + 2.8e-4.  A stop decision T' < 1e-4 can
+// differ from the oracle's only inside this band around 1e-4.
+constexpr float kTBand = 5.0e-8f;          // 1e-4 x 5e-4
+// A flipped stop decision moves the pixel by the contribution of the splat at the flip, w = alpha' T
+// (the whole splat is in or out; after it the pixel stops at the next live splat).  Flips with
+// w <= kJump are left alone (|pixel error| <= kJump + ~1e-6 < tests' BLEND_FAST_TOL = 2e-4); larger
+// ones are replayed exactly.
+constexpr float kJump = 1.0e-4f;
+
+__device__ __forceinline__ void write_pixel(const FrameC &fc, int e, int px, int py, float T, float C0, float C1,
+                                            float C2, void *out_l, void *out_r, int fmt) {
+  const float o0 = __fmaf_rn(T, fc.bg[0], C0);
+  const float o1 = __fmaf_rn(T, fc.bg[1], C1);
+  const float o2 = __fmaf_rn(T, fc.bg[2], C2);
+  void *out = e ? out_r : out_l;
+  const size_t HW = (size_t)fc.width * fc.height, pix = (size_t)py * fc.width + px;
+  if (fmt == 0) {
+    float *o = reinterpret_cast<float *>(out);
+    o[pix] = o0;
+    o[HW + pix] = o1;
+    o[2 * HW + pix] = o2;
+  } else {
+    auto q8 = [](float x) -> uint32_t {
+      float y = fminf(fmaxf(__fmul_rn(x, 255.0f), 0.0f), 255.0f);
+      return (uint32_t)__float2int_rn(y);
+    };
+    reinterpret_cast<uint32_t *>(out)[pix] = q8(o0) | (q8(o1) << 8) | (q8(o2) << 16) | (q8(1.0f - T) << 24);
+  }
+}
+
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 constexpr int kBWarps = kBThreads / 32;
 
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
@@ -45,7 +93,8 @@ __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
              const uint32_t *__restrict__ pair_vals,
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
-             void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
+             void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr,
+             uint32_t *__restrict__ fixup) {
   // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
   // walks all three (offsets 0, 512, 1024 bytes)
   __shared__ float4 slots[kBWarps][96];
@@ -66,17 +115,20 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   rg.x = __shfl_sync(0xFFFFFFFFu, rg.x, 0);   // (uniform by construction; tells the compiler)
   rg.y = __shfl_sync(0xFFFFFFFFu, rg.y, 0);
   float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-  // a lane's liveness floor on power: -inf while it composites, +inf once it has terminated (or lies
-  // outside the image), so nothing is live for it any more (one FMNMX instead of a predicate chain)
-  const float kInf = __int_as_float(0x7F800000);
-  float pfloor = inside ? -kInf : kInf;
+  // bias of the exponent: 0 while the lane composites, -1000 once it has terminated (or lies outside
+  // the image): ex2 then returns 0, so nothing is accepted any more (no predicate on the hot path)
+  float bias = inside ? 0.0f : -1000.0f;
+  float trej = 1.0f;        // T' of the splat the lane stopped before (1: not stopped)
+  float wl = 0.0f;          // contribution alpha' T of the lane's last accepted splat
+  float amarg = 1.0f;       // min over the lane's evaluations of |alpha' - 1/255|
+  float xmax = -1.0f;       // max of the exponent argument: > 0 iff some evaluation had power > 0
   uint32_t nev = 0, nexp = 0;
   uint32_t base = (uint32_t)__cvta_generic_to_shared(&slots[warp][0]);
   asm volatile("" : "+r"(base));   // keep the slot address in a register
   const uint32_t lt = lanemask_lt();
 
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
-    if (__all_sync(0xFFFFFFFFu, pfloor > 0.0f)) break;
+    if (__all_sync(0xFFFFFFFFu, bias < 0.0f)) break;
     const uint32_t idx = b + lane;
     // the pair key's block mask (bit = warp) says whether the splat's box of {power >= skip bound}
     // meets this warp's 8x4 block (computed by project.cu with the fp32 test of DESIGN.md N5)
@@ -93,37 +145,55 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     const uint32_t n = __popc(bits);
     __syncwarp();
     const uint32_t end = base + 16 * n;
-    const bool done0 = pfloor > 0.0f;
+    const bool done0 = bias < 0.0f;
     uint32_t pstop = end;
-#pragma unroll 2
-    for (uint32_t j = 0; j < n; ++j) {   // warp-uniform trip count
+#pragma unroll 4
+    for (uint32_t j = 0; j < n; ++j) {   // warp-uniform trip count, no divergent branch
       const uint32_t p = base + 16 * j;
       const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
       const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
       const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
       const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
-      const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
-      const bool live = power >= fmaxf(q.y, pfloor) && power <= 0.0f;
-      if (!__any_sync(0xFFFFFFFFu, live)) continue;
-      if (kCount) nexp += live;
-      float al = fminf(0.99f, __fmul_rn(q.z, exp_blend(power)));   // garbage (discarded) if !live
-      al = (al >= kAlphaMin) & live ? al : 0.0f;
+      const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));   // N6, the oracle's bits
+      const float x = __fmaf_rn(power, kLog2e, bias);   // > 0 iff power > 0 while the lane composites
+      xmax = fmaxf(xmax, x);               // (3DGS skips power > 0: left to the exact replay)
+      float al = fminf(0.99f, __fmul_rn(q.z, ex2_approx(x)));
+      amarg = fminf(amarg, fabsf(__fsub_rn(al, kAlphaMin)));
+      al = al >= kAlphaMin ? al : 0.0f;
       const float Tn = __fmaf_rn(-al, T, T);
-      const bool term = Tn < 0.0001f;   // terminate before this splat; the rest is not evaluated
-      if (kCount && term) pstop = p;
-      if (!term) {
-        const float w = __fmul_rn(al, T);
-        const float2 gb = lds_f2(p + 1024);
-        C0 = __fmaf_rn(q.w, w, C0);
-        C1 = __fmaf_rn(gb.x, w, C1);
-        C2 = __fmaf_rn(gb.y, w, C2);
-        T = Tn;
+      const bool term = Tn < 0.0001f;      // stop before this splat; the rest is not evaluated
+      if (kCount) {
+        nexp += al > 0.0f && !term;
+        if (term && bias == 0.0f) pstop = p;
       }
-      // pfloor = term ? inf : pfloor as one predicated move (the C form compiles to three)
-      asm("{\n .reg .pred p;\n setp.lt.f32 p, %1, 0f38D1B717;\n @p mov.b32 %0, 0x7F800000;\n}" : "+f"(pfloor) : "f"(Tn));
+      trej = term ? Tn : trej;
+      bias = term ? -1000.0f : bias;
+      const float w = term ? 0.0f : __fmul_rn(al, T);
+      wl = w > 0.0f ? w : wl;
+      const float2 gb = lds_f2(p + 1024);
+      C0 = __fmaf_rn(q.w, w, C0);
+      C1 = __fmaf_rn(gb.x, w, C1);
+      C2 = __fmaf_rn(gb.y, w, C2);
+      T = term ? T : Tn;
     }
-    if (kCount && !done0) nev += (pstop - base) / 16 + (pfloor > 0.0f ? 1 : 0);
+    if (kCount && !done0) nev += (pstop - base) / 16 + (pstop != end ? 1 : 0);
     __syncwarp();
+  }
+  // R5 exactness check: the fast exponential can flip a decision only (i) where alpha' came within
+  // 2^-19 relative of 1/255 (skip), (ii) where power > 0 (skip), (iii) where T' came within kTBand of
+  // 1e-4 (stop) -- for the splat the lane stopped before (trej) or its last accepted one (T) -- and a
+  // stop flip matters only if that splat's contribution exceeds kJump.  Such pixels (rare) go to the
+  // exact replay (blend_fixup_kernel: the oracle's op sequence with exp_s); everywhere else every
+  // decision is the oracle's.
+  const bool redo = inside && (xmax > 0.0f || amarg <= kAlphaGuard ||
+                               (fabsf(__fsub_rn(T, 0.0001f)) <= kTBand && wl > kJump) ||
+                               (fabsf(__fsub_rn(trej, 0.0001f)) <= kTBand && __fsub_rn(T, trej) > kJump));
+  const uint32_t rb = __ballot_sync(0xFFFFFFFFu, redo);
+  if (rb) {
+    uint32_t at = 0;
+    if (lane == 0) at = atomicAdd(&ctr->n_fixup, (uint32_t)__popc(rb));
+    at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    if (redo) fixup[at + __popc(rb & lt)] = ((uint32_t)e << 31) | (uint32_t)(py * fc.width + px);
   }
   if (kCount) {
 #pragma unroll
@@ -136,42 +206,90 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
       atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
     }
   }
-  if (!inside) return;
-  const float o0 = __fmaf_rn(T, fc.bg[0], C0);
-  const float o1 = __fmaf_rn(T, fc.bg[1], C1);
-  const float o2 = __fmaf_rn(T, fc.bg[2], C2);
-  void *out = e ? out_r : out_l;
-  const size_t HW = (size_t)fc.width * fc.height, pix = (size_t)py * fc.width + px;
-  if (fmt == 0) {
-    float *o = reinterpret_cast<float *>(out);
-    o[pix] = o0;
-    o[HW + pix] = o1;
-    o[2 * HW + pix] = o2;
-  } else {
-    auto q8 = [](float x) -> uint32_t {
-      float y = fminf(fmaxf(__fmul_rn(x, 255.0f), 0.0f), 255.0f);
-      return (uint32_t)__float2int_rn(y);
-    };
-    reinterpret_cast<uint32_t *>(out)[pix] = q8(o0) | (q8(o1) << 8) | (q8(o2) << 16) | (q8(1.0f - T) << 24);
+  if (!inside || redo) return;
+  write_pixel(fc, e, px, py, T, C0, C1, C2, out_l, out_r, fmt);
+}
+
+// Exact replay of the flagged pixels: the oracle's per-pixel loop (O-8, N6) with exp_s over
+// the tile's sorted list (the pair key's block bit skips splats whose skip box misses the pixel's 8x4
+// block: decision-preserving, N5).  One warp per pixel: the lanes take 32 consecutive pairs, evaluate
+// power / alpha' / the skip decisions exactly and in parallel, then the accepted ones are composited in
+// order (the T chain is sequential: one shuffle round per accepted splat).
+__global__ void __launch_bounds__(128)
+blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
+                   const uint32_t *__restrict__ pair_vals, const float4 *__restrict__ spA,
+                   const float4 *__restrict__ spB, const float4 *__restrict__ spC, void *__restrict__ out_l,
+                   void *__restrict__ out_r, int fmt, const FrameCounters *__restrict__ ctr,
+                   const uint32_t *__restrict__ fixup) {
+  const uint32_t lane = lane_id();
+  const uint32_t nfix = __shfl_sync(0xFFFFFFFFu, ctr->n_fixup, 0);
+  const uint32_t gw = __shfl_sync(0xFFFFFFFFu, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, 0);
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = gw; k < nfix; k += nw) {
+    const uint32_t code = fixup[k];
+    const int e = (int)(code >> 31);
+    const int pix = (int)(code & 0x7FFFFFFFu);
+    const int px = pix % fc.width, py = pix / fc.width;
+    const int tile = e * fc.Te + (py / kTile) * fc.TW + px / kTile;
+    const uint32_t wbit = 1u << (24 + ((px % kTile) >> 3) + 2 * ((py % kTile) >> 2));
+    const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
+    const uint32_t r0 = ~ranges[tile].x, r1 = ranges[tile].y;
+    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+    bool stop = false;
+    for (uint32_t b = r0; b < r1 && !stop; b += 32) {
+      const uint32_t i = b + lane;
+      bool ok = false;
+      float al = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+      if (i < r1 && (pair_keys[i] & wbit)) {
+        const uint32_t c = pair_vals[i];
+        const float4 a = spA[c], q = spB[c], cc = spC[c];
+        const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
+        const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
+        const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
+        if (!(power > 0.0f)) {
+          al = fminf(0.99f, __fmul_rn(q.z, exp_s(power)));
+          ok = al >= kAlphaMin;
+          cr = q.w; cg = cc.x; cb = cc.y;
+        }
+      }
+      uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+      while (m) {   // warp-uniform
+        const int l = __ffs(m) - 1;
+        m &= m - 1;
+        const float a = __shfl_sync(0xFFFFFFFFu, al, l);
+        const float Tn = __fmaf_rn(-a, T, T);
+        if (Tn < 0.0001f) { stop = true; break; }
+        const float w = __fmul_rn(a, T);
+        C0 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cr, l), w, C0);
+        C1 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cg, l), w, C1);
+        C2 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cb, l), w, C2);
+        T = Tn;
+      }
+    }
+    if (lane == 0) write_pixel(fc, e, px, py, T, C0, C1, C2, out_l, out_r, fmt);
   }
 }
 
 void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_keys, const uint32_t *pair_vals,
-                  const float4 *spA,
-                  const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt, FrameCounters *ctr,
-                  bool count, cudaStream_t st) {
+                  const float4 *spA, const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt,
+                  FrameCounters *ctr, uint32_t *fixup, bool count, int num_sms, cudaStream_t st) {
   const int grid = (fc.ablate & kAblMono) ? fc.Te : 2 * fc.Te;   // GSC_F_MONO: left eye tiles only
   if (count)
-    blend_kernel<true><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<true><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt,
+                                                   ctr, fixup);
   else
-    blend_kernel<false><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr);
+    blend_kernel<false><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt,
+                                                    ctr, fixup);
+  blend_fixup_kernel<<<4 * num_sms, 128, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr,
+                                              fixup);
 }
 
 // elementary-function self test (parity sweeps through the C ABI)
 __global__ void elem_kernel(int fn, const float *__restrict__ in, float *__restrict__ out, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     float x = in[i];
-    out[i] = fn == 0 ? exp_s(x) : fn == 1 ? log_s(x) : fn == 2 ? tanh_s(x) : fn == 3 ? sigmoid_s(x) : exp_blend(x);
+    out[i] = fn == 0 ? exp_s(x) : fn == 1 ? log_s(x) : fn == 2 ? tanh_s(x) : fn == 3 ? sigmoid_s(x)
+             : fn == 4 ? exp_blend(x) : ex2_approx(__fmaf_rn(x, kLog2e, 0.0f));   // 5: the blend's fast exp
   }
 }
 void launch_elem(int fn, const float *in, float *out, size_t n, int num_sms, cudaStream_t st) {

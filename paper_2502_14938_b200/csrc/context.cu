@@ -36,9 +36,11 @@ void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, int,
                  cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
-                  const float4 *,
-                  void *, void *, int, FrameCounters *, bool, cudaStream_t);
+                  const float4 *, void *, void *, int, FrameCounters *, uint32_t *, bool, int, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
+void launch_derive_f32(const float pu[3], const uint32_t *, const float4 *, const float *, const float *, const float *,
+                       const float *, const float *, const float *, const float *, float *, float4 *, FrameCounters *,
+                       int, cudaStream_t);
 int sort_tile_size();
 int emit_tile_size();
 }  // namespace gsc
@@ -86,6 +88,8 @@ struct gsc_ctx {
   DevBuf<float> offs, scale;
   DevBuf<int8_t> W1T, W2T;
   DevBuf<int32_t> b1s, b2s;
+  bool real = false;                 // real-weights scene (F4): fp32 features / weights below
+  DevBuf<float> featf, W1f, b1f, W2f, b2f;   // [N][32], [35][96], [96], [32][110] (heads concatenated), [110]
   // cache
   DevBuf<int32_t> birth;
   DevBuf<uint32_t> vis[2];
@@ -114,12 +118,14 @@ struct gsc_ctx {
   DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list, live_g;
   DevBuf<uint32_t> live_bits;   // live bitset of the visible slots (live_mark -> live)
   DevBuf<uint32_t> pkey_b, pval_b;         // tile-sort scratch (front end only)
+  DevBuf<uint32_t> fixup;                  // blend: pixels for the exact replay (blends run in frame order)
   DevBuf<uint32_t> sort_status_a, sort_status_b;
   size_t zero_bytes = 0, off_cull = 0, off_proj = 0, off_emit = 0;
   DevBuf<FrameRecordDev> rec_dev;
   FrameRecordDev *rec_host = nullptr;    // pinned ring
   FrameSlot slots[kRing];
   int64_t frames_rendered = 0, frames_reported = 0;
+  int64_t frames_checked = 0;            // frames whose capacity overflow flag has been reported
   FrameC fc{};
   float pu[3] = {0, 0, 0};
   cudaStream_t last_stream = nullptr;
@@ -128,6 +134,7 @@ struct gsc_ctx {
   DevBuf<unsigned char> img_dev[2][2];
   static constexpr int kHostRing = 8;
   cudaEvent_t host_done[kHostRing] = {};
+  int64_t host_frame[kHostRing] = {};    // frame sequence number of each in-flight host submission
   int64_t host_submitted = 0;
 
   FrameSet &last_set() { return fs[(frames_rendered + 1) & 1]; }   // the set of the last rendered frame
@@ -240,64 +247,108 @@ static __global__ void fill_i32(int32_t *p, size_t n, int32_t v) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
-static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
+// Exactly one of g (grid codes, R3/R6) and f (real fp32 weights, F4) is non-null.
+static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *g, const gsc_scene_desc_f32 *f) {
+  struct { int32_t n_anchors, lod_levels; float d0; const float *pos, *offs, *scale; const uint8_t *level; } c{};
+  if (g) c = {g->n_anchors, g->lod_levels, g->d0, g->pos, g->offs, g->scale, g->level};
+  else c = {f->n_anchors, f->lod_levels, f->d0, f->pos, f->offs, f->scale, f->level};
+  const auto *s = &c;
   const int N = s->n_anchors;
-  if (N <= 0 || s->lod_levels < 1 || s->lod_levels > 64 || !(s->d0 > 0.0f) || !s->pos || !s->feat || !s->offs ||
-      !s->scale || !s->level || !s->W1 || !s->b1 || !s->W2a || !s->b2a || !s->W2c || !s->b2c || !s->W2s || !s->b2s)
+  const bool wok = g ? (g->feat && g->W1 && g->b1 && g->W2a && g->b2a && g->W2c && g->b2c && g->W2s && g->b2s)
+                     : (f->feat && f->W1 && f->b1 && f->W2a && f->b2a && f->W2c && f->b2c && f->W2s && f->b2s);
+  if (N <= 0 || s->lod_levels < 1 || s->lod_levels > 64 || !(s->d0 > 0.0f) || !s->pos || !s->offs || !s->scale ||
+      !s->level || !wok)
     return fail(ctx, GSC_EINVAL, "invalid scene description");
   if ((int64_t)N * kK >= (1LL << 29)) return fail(ctx, GSC_EINVAL, "scene too large (N*K must be < 2^29)");
   for (int i = 0; i < N; ++i)
     if (s->level[i] >= s->lod_levels) return fail(ctx, GSC_EFORMAT, "anchor level >= L at anchor " + std::to_string(i));
-  // exact int32 range of the grid MLP (R3): |z1| <= hmax, |z2| < 2^31
-  int64_t hmax = 0;
-  for (int n = 0; n < 96; ++n) {
-    int64_t acc = 128 * (int64_t)std::abs((int)s->b1[n]);
-    for (int k = 0; k < kF + 3; ++k) acc += 127 * (int64_t)std::abs((int)s->W1[k * 96 + n]);
-    hmax = std::max(hmax, acc);
-  }
-  if (hmax >= (1LL << 24)) return fail(ctx, GSC_EFORMAT, "hidden activations may exceed 24 bits (3 tensor-core limbs)");
-  std::vector<int8_t> W1T(96 * 36, 0), W2T(kNOut * 32, 0);
-  std::vector<int32_t> b1s(96), b2s(kNOut);
-  for (int n = 0; n < 96; ++n) {
-    for (int k = 0; k < kF + 3; ++k) W1T[n * 36 + k] = s->W1[k * 96 + n];
-    b1s[n] = 128 * (int32_t)s->b1[n];
-  }
-  for (int m = 0; m < kNOut; ++m) {
-    const int8_t *W2; int nh, mm; int8_t b;
-    if (m < kK) { W2 = s->W2a; nh = kK; mm = m; b = s->b2a[mm]; }
-    else if (m < 4 * kK) { W2 = s->W2c; nh = 3 * kK; mm = m - kK; b = s->b2c[mm]; }
-    else { W2 = s->W2s; nh = 7 * kK; mm = m - 4 * kK; b = s->b2s[mm]; }
-    int64_t bound = 16384 * (int64_t)std::abs((int)b);
-    for (int u = 0; u < 32; ++u) {
-      W2T[m * 32 + u] = W2[u * nh + mm];
-      bound += hmax * std::abs((int)W2[u * nh + mm]);
+  std::vector<int8_t> W1T, W2T;
+  std::vector<int32_t> b1s, b2s;
+  std::vector<float> W2f, b2f;
+  if (g) {
+    // exact int32 range of the grid MLP (R3): |z1| <= hmax, |z2| < 2^31
+    int64_t hmax = 0;
+    for (int n = 0; n < 96; ++n) {
+      int64_t acc = 128 * (int64_t)std::abs((int)g->b1[n]);
+      for (int k = 0; k < kF + 3; ++k) acc += 127 * (int64_t)std::abs((int)g->W1[k * 96 + n]);
+      hmax = std::max(hmax, acc);
     }
-    if (bound >= (1LL << 31)) return fail(ctx, GSC_EFORMAT, "decoder weights exceed the exact int32 range");
-    b2s[m] = 16384 * (int32_t)b;
+    if (hmax >= (1LL << 24)) return fail(ctx, GSC_EFORMAT, "hidden activations may exceed 24 bits (3 tensor-core limbs)");
+    W1T.assign(96 * 36, 0); W2T.assign(kNOut * 32, 0); b1s.resize(96); b2s.resize(kNOut);
+    for (int n = 0; n < 96; ++n) {
+      for (int k = 0; k < kF + 3; ++k) W1T[n * 36 + k] = g->W1[k * 96 + n];
+      b1s[n] = 128 * (int32_t)g->b1[n];
+    }
+    for (int m = 0; m < kNOut; ++m) {
+      const int8_t *W2; int nh, mm; int8_t b;
+      if (m < kK) { W2 = g->W2a; nh = kK; mm = m; b = g->b2a[mm]; }
+      else if (m < 4 * kK) { W2 = g->W2c; nh = 3 * kK; mm = m - kK; b = g->b2c[mm]; }
+      else { W2 = g->W2s; nh = 7 * kK; mm = m - 4 * kK; b = g->b2s[mm]; }
+      int64_t bound = 16384 * (int64_t)std::abs((int)b);
+      for (int u = 0; u < 32; ++u) {
+        W2T[m * 32 + u] = W2[u * nh + mm];
+        bound += hmax * std::abs((int)W2[u * nh + mm]);
+      }
+      if (bound >= (1LL << 31)) return fail(ctx, GSC_EFORMAT, "decoder weights exceed the exact int32 range");
+      b2s[m] = 16384 * (int32_t)b;
+    }
+  } else {
+    auto finite = [](const float *p, size_t n) {
+      for (size_t k = 0; k < n; ++k)
+        if (!std::isfinite(p[k])) return false;
+      return true;
+    };
+    if (!finite(f->feat, (size_t)N * kF) || !finite(f->W1, 35 * 96) || !finite(f->b1, 96) ||
+        !finite(f->W2a, 32 * kK) || !finite(f->b2a, kK) || !finite(f->W2c, 32 * 3 * kK) || !finite(f->b2c, 3 * kK) ||
+        !finite(f->W2s, 32 * 7 * kK) || !finite(f->b2s, 7 * kK))
+      return fail(ctx, GSC_EFORMAT, "non-finite feature or decoder weight");
+    // layer-2 weights of the three heads side by side: W2f[u][m], m = alpha 0..9 | colour 10..39 | cov 40..109
+    W2f.assign(32 * kNOut, 0.0f); b2f.resize(kNOut);
+    for (int m = 0; m < kNOut; ++m) {
+      const float *W2; int nh, mm;
+      if (m < kK) { W2 = f->W2a; nh = kK; mm = m; b2f[m] = f->b2a[mm]; }
+      else if (m < 4 * kK) { W2 = f->W2c; nh = 3 * kK; mm = m - kK; b2f[m] = f->b2c[mm]; }
+      else { W2 = f->W2s; nh = 7 * kK; mm = m - 4 * kK; b2f[m] = f->b2s[mm]; }
+      for (int u = 0; u < 32; ++u) W2f[u * kNOut + m] = W2[u * nh + mm];
+    }
   }
   ctx->have_scene = false;
   ctx->N = N; ctx->L = s->lod_levels; ctx->d0 = s->d0;
   const size_t NK = (size_t)N * kK;
   CU(ctx->pos_m.alloc(N));
   CU(ctx->level.alloc(N));
-  CU(ctx->feat.alloc((size_t)N * kF));
   CU(ctx->offs.alloc(NK * 3));
   CU(ctx->scale.alloc((size_t)N * 3));
-  CU(ctx->W1T.alloc(96 * 36));
-  CU(ctx->W2T.alloc(kNOut * 32));
-  CU(ctx->b1s.alloc(96));
-  CU(ctx->b2s.alloc(kNOut));
+  ctx->real = f != nullptr;
+  CU(ctx->W1T.alloc(g ? 96 * 36 : 0));
+  CU(ctx->W2T.alloc(g ? kNOut * 32 : 0));
+  CU(ctx->b1s.alloc(g ? 96 : 0));
+  CU(ctx->b2s.alloc(g ? kNOut : 0));
+  CU(ctx->featf.alloc(f ? (size_t)N * kF : 0));
+  CU(ctx->W1f.alloc(f ? 35 * 96 : 0));
+  CU(ctx->b1f.alloc(f ? 96 : 0));
+  CU(ctx->W2f.alloc(f ? 32 * kNOut : 0));
+  CU(ctx->b2f.alloc(f ? kNOut : 0));
   DevBuf<float> pos;
   CU(pos.alloc((size_t)N * 3));
   CU(cudaMemcpy(pos.p, s->pos, (size_t)N * 12, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->level.p, s->level, N, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(ctx->feat.p, s->feat, (size_t)N * kF, cudaMemcpyHostToDevice));
+  CU(ctx->feat.alloc(g ? (size_t)N * kF : 0));
+  if (g) CU(cudaMemcpy(ctx->feat.p, g->feat, (size_t)N * kF, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->offs.p, s->offs, NK * 12, cudaMemcpyHostToDevice));
   CU(cudaMemcpy(ctx->scale.p, s->scale, (size_t)N * 12, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(ctx->W1T.p, W1T.data(), W1T.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(ctx->W2T.p, W2T.data(), W2T.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(ctx->b1s.p, b1s.data(), 96 * 4, cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(ctx->b2s.p, b2s.data(), kNOut * 4, cudaMemcpyHostToDevice));
+  if (g) {
+    CU(cudaMemcpy(ctx->W1T.p, W1T.data(), W1T.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->W2T.p, W2T.data(), W2T.size(), cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->b1s.p, b1s.data(), 96 * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->b2s.p, b2s.data(), kNOut * 4, cudaMemcpyHostToDevice));
+  } else {
+    CU(cudaMemcpy(ctx->featf.p, f->feat, (size_t)N * kF * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->W1f.p, f->W1, 35 * 96 * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->b1f.p, f->b1, 96 * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->W2f.p, W2f.data(), W2f.size() * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->b2f.p, b2f.data(), kNOut * 4, cudaMemcpyHostToDevice));
+  }
   launch_margin(N, pos.p, ctx->offs.p, ctx->scale.p, ctx->pos_m.p, nullptr);
   CU(cudaGetLastError());
   // cache + per-frame buffers
@@ -335,6 +386,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
   CU(ctx->pair_off.alloc(ctx->cap_splat));
   CU(ctx->list.alloc(std::min<size_t>(2 * ctx->cap_pairs, (1u << 31) - 1)));
   CU(ctx->pkey_b.alloc(ctx->cap_pairs));
+  CU(ctx->fixup.alloc(2 * (size_t)ctx->cfg.width * ctx->cfg.height));
   CU(ctx->pval_b.alloc(ctx->cap_pairs));
   const int TW = (ctx->cfg.width + 15) / 16, TH = (ctx->cfg.height + 15) / 16;
   for (auto &S : ctx->fs) {
@@ -356,6 +408,10 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *s) {
     CU(S.zero_region.alloc(ctx->zero_bytes));
     CU(cudaMemset(S.zero_region.p, 0, ctx->zero_bytes));
   }
+  // device staging images of the host-buffer calls (either format; per frame parity and eye)
+  for (auto &par : ctx->img_dev)
+    for (auto &im : par)
+      if (im.n < (size_t)ctx->cfg.width * ctx->cfg.height * 12) CU(im.alloc((size_t)ctx->cfg.width * ctx->cfg.height * 12));
   CU(cudaDeviceSynchronize());
   ctx->have_scene = true;
   return reset_cache(ctx, nullptr);
@@ -390,7 +446,9 @@ static gsc_status load_file(gsc_ctx *ctx, const char *path) {
   if (std::memcmp(buf.data(), "GSC2", 4) != 0) return fail(ctx, GSC_EFORMAT, "bad magic at offset 0");
   uint32_t u[6];
   std::memcpy(u, buf.data() + 4, 24);
-  if (u[0] != 2) return fail(ctx, GSC_EFORMAT, "unsupported version at offset 4");
+  if (u[0] != 2 && u[0] != 3) return fail(ctx, GSC_EFORMAT, "unsupported version at offset 4");
+  const bool real = u[0] == 3;   // version 3: fp32 features and decoder weights (F4)
+  const size_t q = real ? 4 : 1;
   const uint32_t N = u[1], F = u[2], K = u[3], L = u[4], H = u[5];
   if (F != (uint32_t)kF || K != (uint32_t)kK || H != (uint32_t)kH)
     return fail(ctx, GSC_EFORMAT, "unsupported F/K/H at offset 12 (need 32/10/32)");
@@ -403,32 +461,72 @@ static gsc_status load_file(gsc_ctx *ctx, const char *path) {
     off += bytes;
     return true;
   };
-  gsc_scene_desc s{};
-  s.n_anchors = (int32_t)N; s.lod_levels = (int32_t)L; s.d0 = d0;
-  const void *p;
-  struct { size_t bytes; const void **dst; } items[] = {
-      {N * 12ull, (const void **)&s.pos}, {N * 32ull, (const void **)&s.feat}, {N * 120ull, (const void **)&s.offs},
-      {N * 12ull, (const void **)&s.scale}, {N * 1ull, (const void **)&s.level}, {35 * 96ull, (const void **)&s.W1},
-      {96ull, (const void **)&s.b1}, {32 * 10ull, (const void **)&s.W2a}, {10ull, (const void **)&s.b2a},
-      {32 * 30ull, (const void **)&s.W2c}, {30ull, (const void **)&s.b2c}, {32 * 70ull, (const void **)&s.W2s},
-      {70ull, (const void **)&s.b2s}};
-  for (auto &it : items) {
-    if (!take(it.bytes, "", &p)) return fail(ctx, GSC_EFORMAT, "truncated at offset " + std::to_string(off));
-    *it.dst = p;
+  const void *p[13];
+  const size_t bytes[13] = {N * 12ull, N * 32ull * q, N * 120ull, N * 12ull, N * 1ull, 35 * 96ull * q, 96ull * q,
+                            32 * 10ull * q, 10ull * q, 32 * 30ull * q, 30ull * q, 32 * 70ull * q, 70ull * q};
+  for (int k = 0; k < 13; ++k)
+    if (!take(bytes[k], "", &p[k])) return fail(ctx, GSC_EFORMAT, "truncated at offset " + std::to_string(off));
+  // (the file buffer is char-aligned: copy the f32 / int8 arrays through vectors of their type)
+  auto fv = [&](int k) { std::vector<float> v(bytes[k] / 4); std::memcpy(v.data(), p[k], bytes[k]); return v; };
+  std::vector<float> pos = fv(0), offs = fv(2), scale = fv(3);
+  if (real) {
+    std::vector<float> w[13];
+    for (int k : {1, 5, 6, 7, 8, 9, 10, 11, 12}) w[k] = fv(k);
+    gsc_scene_desc_f32 d{(int32_t)N, (int32_t)L, d0, pos.data(), w[1].data(), offs.data(), scale.data(),
+                         (const uint8_t *)p[4], w[5].data(), w[6].data(), w[7].data(), w[8].data(), w[9].data(),
+                         w[10].data(), w[11].data(), w[12].data()};
+    return upload_scene(ctx, nullptr, &d);
   }
-  return upload_scene(ctx, &s);
+  gsc_scene_desc d{};
+  d.n_anchors = (int32_t)N; d.lod_levels = (int32_t)L; d.d0 = d0;
+  d.pos = pos.data(); d.feat = (const int8_t *)p[1]; d.offs = offs.data(); d.scale = scale.data();
+  d.level = (const uint8_t *)p[4]; d.W1 = (const int8_t *)p[5]; d.b1 = (const int8_t *)p[6];
+  d.W2a = (const int8_t *)p[7]; d.b2a = (const int8_t *)p[8]; d.W2c = (const int8_t *)p[9];
+  d.b2c = (const int8_t *)p[10]; d.W2s = (const int8_t *)p[11]; d.b2s = (const int8_t *)p[12];
+  return upload_scene(ctx, &d, nullptr);
 }
 
 // ----------------------------------------------------------------------------------- frame
+// Streams and events, created once at gsc_create (nothing is created or allocated inside a frame).
 static gsc_status ensure_streams(gsc_ctx *ctx) {
   if (ctx->sA) return GSC_OK;
   // (stream priorities were measured to make no difference: the two stages share every SM)
   CU(cudaStreamCreateWithFlags(&ctx->sA, cudaStreamNonBlocking));
   CU(cudaStreamCreateWithFlags(&ctx->sB, cudaStreamNonBlocking));
+  CU(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   for (int k = 0; k < 2; ++k) {
     CU(cudaEventCreateWithFlags(&ctx->ev_user[k], cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->ev_a[k], cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->ev_b[k], cudaEventDisableTiming));
+  }
+  for (auto &e : ctx->host_done) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  return GSC_OK;
+}
+
+// Capacity overflows of frames rendered without a stats request are reported (GSC_ECAPACITY, naming the
+// frame) by the next call that knows the frame finished: gsc_render_pair (non-blocking, from the
+// blend-done events), gsc_sync, gsc_wait_frame, gsc_render_pair_host.  Each overflowed frame is
+// reported once.
+static gsc_status check_done(gsc_ctx *ctx, int64_t upto) {
+  if (upto - ctx->frames_checked > kRing) ctx->frames_checked = upto - kRing;   // (ring overwritten)
+  while (ctx->frames_checked < upto) {
+    const int64_t f = ctx->frames_checked++;
+    const FrameRecordDev &r = ctx->rec_host[f % kRing];
+    if (r.overflow)
+      return fail(ctx, GSC_ECAPACITY, "frame " + std::to_string(f) + " exceeded the pair capacity (needed " +
+                                          std::to_string(r.n_pairs_raw) + " pairs); its image is incomplete");
+  }
+  return GSC_OK;
+}
+
+static gsc_status check_finished_nonblocking(gsc_ctx *ctx) {
+  for (int64_t back = 1; back <= 2 && back <= ctx->frames_rendered; ++back) {
+    const int64_t f = ctx->frames_rendered - back;
+    if (f < ctx->frames_checked) break;
+    const cudaError_t q = cudaEventQuery(ctx->ev_b[f & 1]);   // last recorded by frame f
+    if (q == cudaSuccess) return check_done(ctx, f + 1);
+    if (q != cudaErrorNotReady) return fail(ctx, GSC_ECUDA, std::string("cudaEventQuery: ") + cudaGetErrorString(q));
+    if (cudaPeekAtLastError() == cudaErrorNotReady) (void)cudaGetLastError();
   }
   return GSC_OK;
 }
@@ -442,7 +540,10 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   if (!ctx->have_scene || !ctx->have_pose) return fail(ctx, GSC_ESTATE, "render before load_scene/set_pose");
   if (!out_l || !out_r || (fmt != GSC_FMT_RGB_F32_PLANAR && fmt != GSC_FMT_RGBA8))
     return fail(ctx, GSC_EINVAL, "bad output buffers or format");
-  if (ensure_streams(ctx) != GSC_OK) return GSC_ECUDA;
+  {
+    const gsc_status cs = check_finished_nonblocking(ctx);
+    if (cs != GSC_OK) return cs;
+  }
   ctx->last_stream = st;
   const int slot_i = (int)(ctx->frames_rendered % kRing);
   const int k = (int)(ctx->frames_rendered & 1);
@@ -474,9 +575,13 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
               ctr, ctx->policy.p, ctx->rec_dev.p + slot_i, sA);
   mark(sA);
   // a3
-  launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p, ctx->b1s.p,
-                ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms,
-                (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, sA);
+  if (ctx->real)   // F4: fixed-order fp32 MLP on the CUDA cores
+    launch_derive_f32(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->featf.p, ctx->offs.p, ctx->scale.p, ctx->W1f.p,
+                      ctx->b1f.p, ctx->W2f.p, ctx->b2f.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, sA);
+  else
+    launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p,
+                  ctx->b1s.p, ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms,
+                  (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, sA);
   mark(sA);
   // a4
   SplatBufs sb{S.spA.p, S.spB.p, S.spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
@@ -507,8 +612,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   CU(cudaStreamWaitEvent(sB, ctx->ev_a[k], 0));
   CU(cudaStreamWaitEvent(sB, ctx->ev_user[k], 0));
   mark(sB);
-  launch_blend(fc, S.ranges.p, S.pkey.p, S.pval.p, S.spA.p, S.spB.p, S.spC.p, out_l, out_r, fmt, ctr,
-               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, sB);
+  launch_blend(fc, S.ranges.p, S.pkey.p, S.pval.p, S.spA.p, S.spB.p, S.spC.p, out_l, out_r, fmt, ctr, ctx->fixup.p,
+               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, ctx->num_sms, sB);
   launch_record(ctr, ctx->rec_dev.p + slot_i, sB);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
                      sB));
@@ -537,6 +642,8 @@ static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
   s->overflow = r.overflow;
   s->n_evals = r.n_evals;
   s->n_exp = r.n_exp;
+  s->n_nonfinite_skipped = r.n_nonfinite;
+  s->n_blend_fixup = r.n_fixup;
   s->depth_used = r.depth_used;
   s->depth_next = r.depth_next;
   s->update_rate = r.n_visible ? (float)r.n_miss / (float)r.n_visible : 0.0f;
@@ -575,6 +682,7 @@ gsc_status gsc_create(int cuda_device, const gsc_config *cfg, gsc_ctx **out) {
   CU(ctx->rec_dev.alloc(kRing));
   CU(cudaMallocHost(&ctx->rec_host, kRing * sizeof(FrameRecordDev)));
   std::memset(ctx->rec_host, 0, kRing * sizeof(FrameRecordDev));
+  if (ensure_streams(ctx) != GSC_OK) return GSC_ECUDA;
   *out = c.release();
   return GSC_OK;
 }
@@ -588,7 +696,13 @@ gsc_status gsc_load_scene(gsc_ctx *ctx, const char *path) {
 gsc_status gsc_load_scene_host(gsc_ctx *ctx, const gsc_scene_desc *scene) {
   if (!ctx || !scene) return GSC_EINVAL;
   CU(cudaSetDevice(ctx->device));
-  return upload_scene(ctx, scene);
+  return upload_scene(ctx, scene, nullptr);
+}
+
+gsc_status gsc_load_scene_host_f32(gsc_ctx *ctx, const gsc_scene_desc_f32 *scene) {
+  if (!ctx || !scene) return GSC_EINVAL;
+  CU(cudaSetDevice(ctx->device));
+  return upload_scene(ctx, nullptr, scene);
 }
 
 gsc_status gsc_set_pose(gsc_ctx *ctx, const gsc_rig *rig) {
@@ -609,7 +723,7 @@ gsc_status gsc_render_pair(gsc_ctx *ctx, void *out_left, void *out_right, int ou
     CU(cudaStreamSynchronize(st));
     fill_stats(ctx, ctx->frames_rendered - 1, stats);
     ctx->frames_reported = ctx->frames_rendered;
-    if (stats->overflow) return fail(ctx, GSC_ECAPACITY, "pair capacity exceeded: needed " + std::to_string(stats->n_pairs));
+    return check_done(ctx, ctx->frames_rendered);
   }
   return GSC_OK;
 }
@@ -620,14 +734,8 @@ static gsc_status render_host_enqueue(gsc_ctx *ctx, const gsc_rig *rig, void *ho
   if (out_format != GSC_FMT_RGB_F32_PLANAR && out_format != GSC_FMT_RGBA8) return GSC_EINVAL;
   gsc_status s = gsc_set_pose(ctx, rig);
   if (s != GSC_OK) return s;
-  if (!ctx->own_stream) CU(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking));
   const size_t bytes = (size_t)ctx->cfg.width * ctx->cfg.height * (out_format == GSC_FMT_RGBA8 ? 4 : 12);
-  auto &img = ctx->img_dev[ctx->frames_rendered & 1];
-  for (int e = 0; e < 2; ++e)
-    if (img[e].n < bytes) {
-      CU(cudaDeviceSynchronize());   // (re)allocation only when the format grows
-      CU(img[e].alloc(bytes));
-    }
+  auto &img = ctx->img_dev[ctx->frames_rendered & 1];   // allocated at scene load for either format
   s = render(ctx, img[0].p, img[1].p, out_format, ctx->own_stream);
   if (s != GSC_OK) return s;
   CU(cudaMemcpyAsync(host_left, img[0].p, bytes, cudaMemcpyDeviceToHost, ctx->own_stream));
@@ -642,11 +750,8 @@ gsc_status gsc_render_pair_host(gsc_ctx *ctx, const gsc_rig *rig, void *host_lef
   gsc_status s = render_host_enqueue(ctx, rig, host_left, host_right, out_format);
   if (s != GSC_OK) return s;
   CU(cudaStreamSynchronize(ctx->own_stream));
-  if (stats) {
-    fill_stats(ctx, ctx->frames_rendered - 1, stats);
-    if (stats->overflow) return fail(ctx, GSC_ECAPACITY, "pair capacity exceeded");
-  }
-  return GSC_OK;
+  if (stats) fill_stats(ctx, ctx->frames_rendered - 1, stats);
+  return check_done(ctx, ctx->frames_rendered);
 }
 
 gsc_status gsc_render_pair_host_async(gsc_ctx *ctx, const gsc_rig *rig, void *host_left, void *host_right,
@@ -655,11 +760,11 @@ gsc_status gsc_render_pair_host_async(gsc_ctx *ctx, const gsc_rig *rig, void *ho
   CU(cudaSetDevice(ctx->device));
   const int64_t q = ctx->host_submitted;
   auto &ev = ctx->host_done[q % gsc_ctx::kHostRing];
-  if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  else CU(cudaEventSynchronize(ev));   // the ring slot's previous frame (kHostRing in flight at most)
+  if (q >= gsc_ctx::kHostRing) CU(cudaEventSynchronize(ev));   // the slot's previous frame (kHostRing in flight)
   gsc_status s = render_host_enqueue(ctx, rig, host_left, host_right, out_format);
   if (s != GSC_OK) return s;
   CU(cudaEventRecord(ev, ctx->own_stream));
+  ctx->host_frame[q % gsc_ctx::kHostRing] = ctx->frames_rendered - 1;
   *seq = q;
   ++ctx->host_submitted;
   return GSC_OK;
@@ -670,7 +775,7 @@ gsc_status gsc_wait_frame(gsc_ctx *ctx, long long seq) {
   CU(cudaSetDevice(ctx->device));
   if (seq + gsc_ctx::kHostRing <= ctx->host_submitted) return GSC_OK;   // its slot was already waited for
   CU(cudaEventSynchronize(ctx->host_done[seq % gsc_ctx::kHostRing]));
-  return GSC_OK;
+  return check_done(ctx, ctx->host_frame[seq % gsc_ctx::kHostRing] + 1);
 }
 
 gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream) {
@@ -680,7 +785,7 @@ gsc_status gsc_sync(gsc_ctx *ctx, void *cuda_stream) {
   if (ctx->own_stream) CU(cudaStreamSynchronize(ctx->own_stream));
   if (ctx->sA) CU(cudaStreamSynchronize(ctx->sA));
   if (ctx->sB) CU(cudaStreamSynchronize(ctx->sB));
-  return GSC_OK;
+  return check_done(ctx, ctx->frames_rendered);
 }
 
 gsc_status gsc_stats_history(gsc_ctx *ctx, gsc_frame_stats *dst, int max, int *n) {
@@ -816,7 +921,7 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
 }
 
 gsc_status gsc_selftest_elementary(gsc_ctx *ctx, int fn, const float *dev_in, float *dev_out, size_t n) {
-  if (!ctx || fn < 0 || fn > 4 || (n && (!dev_in || !dev_out))) return GSC_EINVAL;
+  if (!ctx || fn < 0 || fn > 5 || (n && (!dev_in || !dev_out))) return GSC_EINVAL;
   CU(cudaSetDevice(ctx->device));
   launch_elem(fn, dev_in, dev_out, n, ctx->num_sms, nullptr);
   CU(cudaGetLastError());

@@ -227,7 +227,9 @@ __global__ void record_kernel(const FrameCounters *ctr, FrameRecordDev *rec) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   rec->n_splat = ctr->n_splat;
   rec->n_pairs_raw = ctr->n_pairs_raw;
-  rec->overflow = ctr->overflow;
+  rec->overflow = ctr->overflow | ctr->list_overflow;
+  rec->n_nonfinite = ctr->n_nonfinite;
+  rec->n_fixup = ctr->n_fixup;
   rec->n_evals = ctr->n_evals;
   rec->n_exp = ctr->n_exp;
 }

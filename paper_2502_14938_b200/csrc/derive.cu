@@ -19,6 +19,7 @@
 //    16-byte core matrices), MMAs issued by one thread, completion through
 //    tcgen05.commit -> mbarrier.
 //  derive_kernel (GSC_F_DERIVE_CUDA_CORES): the same integers by dp4a/IMAD.
+//  derive_f32_kernel: the real-weights path (F4): fixed-order fp32 on the CUDA cores (below).
 //
 // Epilogue (Eq. 2), one thread per (anchor, Gaussian):
 //   alpha = tanh_s (kept if > 0), rgb = sigmoid_s, S = s (.) sigmoid_s,
@@ -186,6 +187,102 @@ __global__ void __launch_bounds__(kDThreads) derive_kernel(DeriveArgs p) {
     __syncthreads();
     for (int e = t; e < na * kK; e += kDThreads) {
       int a = e / kK, j = e - a * kK;
+      derive_gaussian(S.o[a], j, S.anchor[a], p.pos_m, p.offs, p.scale, p.alpha, p.pool);
+    }
+  }
+}
+
+// ------------------------------------------------------------------ real-weights kernel (F4, fp32)
+// MLP_theta(f_i, d_view) (Eq. 3) with trained-style fp32 weights, the
+// continuous view direction d_view = v / |v| (v = p_i - p_u, three IEEE divisions, 0 at the camera),
+// and the fixed summation order of DESIGN.md F4 -- every output from its bias, inputs in ascending
+// index order, one fma per term -- so the CUDA cores reproduce the oracle's orc_mlp_f32 bit for bit.
+// (A tensor-core contraction would change the rounding: tf32 / bf16 operands are not fp32, and the
+// MMA's accumulation order is not the written one.)  64 anchors per CTA iteration: layer 1 as
+// 64 x 96 outputs (thread = (anchor, hidden unit), weights W1[k][n] read conflict-free across n,
+// inputs broadcast), layer 2 as 64 x 110 outputs, then the shared epilogue (derive_gaussian).
+struct DeriveF32Args {
+  float pu0, pu1, pu2;
+  const uint32_t *misses;
+  const float4 *pos_m;
+  const float *feat;     // [N][32]
+  const float *offs, *scale;
+  const float *W1;       // [35][96]
+  const float *b1;       // [96]
+  const float *W2;       // [32][110] (heads side by side: alpha 0..9 | colour 10..39 | covariance 40..109)
+  const float *b2;       // [110]
+  float *alpha;
+  float4 *pool;
+  FrameCounters *ctr;
+};
+
+constexpr int kFA = 64;   // anchors per CTA iteration
+
+struct DeriveF32Smem {
+  float W1[kF + 3][96];
+  float b1[96];
+  float W2[kH][kNOut];
+  float b2[kNOut];
+  float x[kFA][kF + 4];      // inputs (32 features, d_view; padded row)
+  float hid[kFA][96 + 1];
+  float o[kFA][kNOut + 1];
+  uint32_t anchor[kFA];
+  uint32_t base;
+};
+
+__global__ void __launch_bounds__(kDThreads) derive_f32_kernel(DeriveF32Args p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  DeriveF32Smem &S = *reinterpret_cast<DeriveF32Smem *>(smem_raw);
+  const int t = threadIdx.x;
+  for (int w = t; w < (kF + 3) * 96; w += kDThreads) (&S.W1[0][0])[w] = p.W1[w];
+  for (int w = t; w < 96; w += kDThreads) S.b1[w] = p.b1[w];
+  for (int w = t; w < kH * kNOut; w += kDThreads) (&S.W2[0][0])[w] = p.W2[w];
+  for (int w = t; w < kNOut; w += kDThreads) S.b2[w] = p.b2[w];
+  const uint32_t M = p.ctr->n_miss;
+  for (;;) {
+    __syncthreads();
+    if (t == 0) S.base = atomicAdd(&p.ctr->tile_derive, 1u) * kFA;
+    __syncthreads();
+    const uint32_t base = S.base;
+    if (base >= M) break;
+    const int na = min((uint32_t)kFA, M - base);
+    if (t < kFA) {
+      const uint32_t i = t < na ? p.misses[base + t] : 0u;
+      S.anchor[t] = i;
+      const float4 pm = p.pos_m[i];
+      const float v0 = __fsub_rn(pm.x, p.pu0), v1 = __fsub_rn(pm.y, p.pu1), v2 = __fsub_rn(pm.z, p.pu2);
+      const float n = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)), __fmul_rn(v2, v2)));
+      S.x[t][kF + 0] = n == 0.0f ? 0.0f : __fdiv_rn(v0, n);
+      S.x[t][kF + 1] = n == 0.0f ? 0.0f : __fdiv_rn(v1, n);
+      S.x[t][kF + 2] = n == 0.0f ? 0.0f : __fdiv_rn(v2, n);
+    }
+    for (int w = t; w < kFA * (kF / 4); w += kDThreads) {   // features: one float4 per thread
+      const int a = w / (kF / 4), c4 = w % (kF / 4);
+      const float4 f = a < na ? reinterpret_cast<const float4 *>(p.feat)[(size_t)p.misses[base + a] * (kF / 4) + c4]
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+      S.x[a][4 * c4 + 0] = f.x; S.x[a][4 * c4 + 1] = f.y; S.x[a][4 * c4 + 2] = f.z; S.x[a][4 * c4 + 3] = f.w;
+    }
+    __syncthreads();
+    for (int o = t; o < kFA * 96; o += kDThreads) {
+      const int a = o / 96, n = o - a * 96;
+      float acc = S.b1[n];
+#pragma unroll
+      for (int k = 0; k < kF + 3; ++k) acc = __fmaf_rn(S.W1[k][n], S.x[a][k], acc);
+      S.hid[a][n] = acc > 0.0f ? acc : 0.0f;   // ReLU
+    }
+    __syncthreads();
+    for (int o = t; o < kFA * kNOut; o += kDThreads) {
+      const int a = o / kNOut, m = o - a * kNOut;
+      const int h = m < kK ? 0 : (m < 4 * kK ? 1 : 2);
+      const float *hp = &S.hid[a][h * kH];
+      float acc = S.b2[m];
+#pragma unroll
+      for (int u = 0; u < kH; ++u) acc = __fmaf_rn(S.W2[u][m], hp[u], acc);
+      S.o[a][m] = acc;
+    }
+    __syncthreads();
+    for (int e = t; e < na * kK; e += kDThreads) {
+      const int a = e / kK, j = e - a * kK;
       derive_gaussian(S.o[a], j, S.anchor[a], p.pos_m, p.offs, p.scale, p.alpha, p.pool);
     }
   }
@@ -441,7 +538,21 @@ __global__ void __launch_bounds__(kMThreads, 1) derive_mma_kernel(DeriveArgs p) 
   }
 }
 
-static int g_derive_grid = 0, g_mma_grid = 0;
+static PerDevice<int> g_mma_grid, g_derive_grid, g_f32_grid;
+
+void launch_derive_f32(const float pu[3], const uint32_t *misses, const float4 *pos_m, const float *feat,
+                       const float *offs, const float *scale, const float *W1, const float *b1, const float *W2,
+                       const float *b2, float *alpha, float4 *pool, FrameCounters *ctr, int num_sms, cudaStream_t st) {
+  DeriveF32Args a{pu[0], pu[1], pu[2], misses, pos_m, feat, offs, scale, W1, b1, W2, b2, alpha, pool, ctr};
+  const int smem = (int)sizeof(DeriveF32Smem);
+  const int grid = g_f32_grid.get([&](int &grid) {
+    cudaFuncSetAttribute(derive_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, derive_f32_kernel, kDThreads, smem);
+    grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  });
+  derive_f32_kernel<<<grid, kDThreads, smem, st>>>(a);
+}
 
 void launch_derive(const float pu[3], const uint32_t *misses, const float4 *pos_m, const int8_t *feat,
                    const float *offs, const float *scale, const int8_t *W1T, const int32_t *b1s, const int8_t *W2T,
@@ -450,21 +561,21 @@ void launch_derive(const float pu[3], const uint32_t *misses, const float4 *pos_
   DeriveArgs a{pu[0], pu[1], pu[2], misses, pos_m, feat, offs, scale, W1T, b1s, W2T, b2s, alpha, pool, ctr};
   if (use_mma) {
     const int smem = (int)sizeof(MmaSmem) + 1024;
-    if (g_mma_grid == 0) {
+    const int grid = g_mma_grid.get([&](int &grid) {
       cudaFuncSetAttribute(derive_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-      g_mma_grid = num_sms;   // one CTA per SM: each owns all 512 TMEM columns
-    }
-    derive_mma_kernel<<<g_mma_grid, kMThreads, smem, st>>>(a);
+      grid = num_sms;   // one CTA per SM: each owns all 512 TMEM columns
+    });
+    derive_mma_kernel<<<grid, kMThreads, smem, st>>>(a);
     return;
   }
   const int smem = (int)sizeof(DeriveSmem);
-  if (g_derive_grid == 0) {
+  const int grid = g_derive_grid.get([&](int &grid) {
     cudaFuncSetAttribute(derive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, derive_kernel, kDThreads, smem);
-    g_derive_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  derive_kernel<<<g_derive_grid, kDThreads, smem, st>>>(a);
+    grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  });
+  derive_kernel<<<grid, kDThreads, smem, st>>>(a);
 }
 
 }  // namespace gsc

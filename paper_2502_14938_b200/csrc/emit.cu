@@ -44,7 +44,10 @@ __global__ void __launch_bounds__(kXThreads)
 pairoff_reduce_kernel(EmitIn in, uint32_t *__restrict__ agg, const FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_w[kXThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t C = ctr->n_splat;
+  // when project's kept-tile list overflowed (list_overflow) the lists are incomplete: the frame then
+  // has no pairs (n_pairs stays 0, an empty image; nothing reads the list out of bounds) and reports
+  // GSC_ECAPACITY
+  const uint32_t C = ctr->list_overflow ? 0u : ctr->n_splat;
   const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     uint32_t cnt[kOffItems], sum = 0;
@@ -68,7 +71,10 @@ __global__ void __launch_bounds__(kXThreads)
 pairoff_scan_kernel(EmitIn in, uint32_t cap, const uint32_t *__restrict__ agg, FrameCounters *__restrict__ ctr) {
   __shared__ uint32_t s_cnt[kXThreads / 32], s_pre[kXThreads / 32];
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
-  const uint32_t C = ctr->n_splat;
+  // when project's kept-tile list overflowed (list_overflow) the lists are incomplete: the frame then
+  // has no pairs (n_pairs stays 0, an empty image; nothing reads the list out of bounds) and reports
+  // GSC_ECAPACITY
+  const uint32_t C = ctr->list_overflow ? 0u : ctr->n_splat;
   const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
@@ -174,22 +180,23 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   }
 }
 
-static int g_red_grid = 0, g_scan_grid = 0, g_exp_grid = 0;
+struct EmitGrids { int red, scan, exp; };
+static PerDevice<EmitGrids> g_emit;
 
 void launch_emit(const EmitIn &in, uint32_t cap, uint32_t *keys_out, uint32_t *vals_out, uint32_t *status,
                  FrameCounters *ctr, int tbits, int num_sms, cudaStream_t st) {
-  if (!g_scan_grid) {
+  const EmitGrids &g = g_emit.get([&](EmitGrids &g) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_reduce_kernel, kXThreads, 0);
-    g_red_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    g.red = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, pairoff_scan_kernel, kXThreads, 0);
-    g_scan_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    g.scan = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, expand_kernel, kXThreads, 0);
-    g_exp_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  pairoff_reduce_kernel<<<g_red_grid, kXThreads, 0, st>>>(in, status, ctr);
-  pairoff_scan_kernel<<<g_scan_grid, kXThreads, 0, st>>>(in, cap, status, ctr);
-  expand_kernel<<<g_exp_grid, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr, (uint32_t)tbits);
+    g.exp = num_sms * (per_sm > 0 ? per_sm : 1);
+  });
+  pairoff_reduce_kernel<<<g.red, kXThreads, 0, st>>>(in, status, ctr);
+  pairoff_scan_kernel<<<g.scan, kXThreads, 0, st>>>(in, cap, status, ctr);
+  expand_kernel<<<g.exp, kXThreads, 0, st>>>(in, keys_out, vals_out, ctr, (uint32_t)tbits);
 }
 
 int emit_tile_size() { return kOffTile; }

@@ -5,6 +5,7 @@
 // __fmaf_rn is spelled out).
 #pragma once
 #include <cstdint>
+#include <mutex>
 #include <cuda_runtime.h>
 
 namespace gsc {
@@ -48,7 +49,11 @@ struct FrameCounters {
   uint32_t list_top;           // project: bump allocator of the kept-tile list
   unsigned long long n_evals;  // blend: (pixel, splat) evaluations executed
   unsigned long long n_exp;    // blend: evaluations that reached exp_s
-  uint32_t tile_pairoff, tile_expand, pad2[2];
+  uint32_t tile_pairoff, tile_expand;
+  uint32_t list_overflow;      // project: the kept-tile list ran out (the frame's pairs are dropped)
+  uint32_t n_nonfinite;        // project: (Gaussian, eye) skipped for non-finite parameters
+  uint32_t n_fixup;            // blend: pixels sent to the exact replay (R5 guard bands)
+  uint32_t pad3[3];
   uint32_t hist_depth[4][256];
   uint32_t hist_tile[2][256];
 };
@@ -91,8 +96,26 @@ struct EmitIn {
 // snapshot copied to host every frame
 struct FrameRecordDev {
   int32_t frame, depth_used, depth_next, pad0;
-  uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, pad1, pad2;
+  uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, n_nonfinite, n_fixup;
   unsigned long long n_evals, n_exp;
+};
+
+// Launch configuration kept per CUDA device (grid sizes from the device's occupancy, the
+// MaxDynamicSharedMemorySize opt-ins, which are per-device attributes), initialised once per device,
+// thread-safe: contexts on several devices of one process each get their own.
+constexpr int kMaxDevices = 64;
+template <typename T>
+struct PerDevice {
+  T v[kMaxDevices]{};
+  std::once_flag once[kMaxDevices];
+  template <typename Init>
+  T &get(Init init) {
+    int d = 0;
+    cudaGetDevice(&d);
+    if (d < 0 || d >= kMaxDevices) d = 0;
+    std::call_once(once[d], [&] { init(v[d]); });
+    return v[d];
+  }
 };
 
 // ---------------------------------------------------------------- helpers

@@ -34,13 +34,19 @@ struct SplatOut {
   float depth;
 };
 
+// returns 1: projected (o filled); 0: culled; -1: skipped for non-finite parameters ("non-finite
+// splat parameters -> skip splat, count in FrameRecord diagnostics"): a non-finite mean or covariance
+// entry, or a non-finite 2D covariance / determinant / conic / centre of a Gaussian in the depth range.
 template <int kAbl>
-__device__ __forceinline__ bool project_one(const EyeC &ec, int width, int height, int TW, int TH, float r2s,
-                                            const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
+__device__ __forceinline__ int project_one(const EyeC &ec, int width, int height, int TW, int TH, float r2s,
+                                           const float4 &p0, const float4 &p1, const float4 &p2, SplatOut &o) {
   // (the live test 255 alpha > 1 was made by live_kernel; r2s = 2 ln(255 alpha) is eye-independent)
+  if (!isfinite(p0.x) || !isfinite(p0.y) || !isfinite(p0.z) || !isfinite(p0.w) || !isfinite(p1.x) ||
+      !isfinite(p1.y) || !isfinite(p1.z) || !isfinite(p1.w) || !isfinite(p2.x))
+    return -1;
   float t0 = __fsub_rn(p0.x, ec.p[0]), t1 = __fsub_rn(p0.y, ec.p[1]), t2 = __fsub_rn(p0.z, ec.p[2]);
   float x = dot3(t0, t1, t2, ec.r0), y = dot3(t0, t1, t2, ec.r1), z = dot3(t0, t1, t2, ec.r2);
-  if (!(z > ec.near_plane) || z > ec.far_plane) return false;
+  if (!(z > ec.near_plane) || z > ec.far_plane) return 0;
   // N8: one reciprocal of z (and of det below), rounded once, multiplied in
   const float iz = __fdiv_rn(1.0f, z), iz2 = __fmul_rn(iz, iz);
   float xz = __fmul_rn(x, iz), yz = __fmul_rn(y, iz);
@@ -69,7 +75,8 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   a = __fadd_rn(a, 0.3f);
   c = __fadd_rn(c, 0.3f);
   float det = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, b));
-  if (!(det > 0.0f)) return false;
+  if (!isfinite(det)) return -1;
+  if (!(det > 0.0f)) return 0;
   o.sxx = a;
   o.syy = c;
   const float idet = __fdiv_rn(1.0f, det);
@@ -84,18 +91,18 @@ __device__ __forceinline__ bool project_one(const EyeC &ec, int width, int heigh
   o.thr = __fadd_rn(__fmul_rn(r2, kKappa), kSlack);
   o.depth = z;
   if (!isfinite(o.A) || !isfinite(o.B) || !isfinite(o.C) || !isfinite(o.u) || !isfinite(o.v) || !isfinite(o.thr))
-    return false;
+    return -1;
   float ex = __fadd_rn(__fsqrt_rn(__fmul_rn(o.thr, a)), 1.0f), ey = __fadd_rn(__fsqrt_rn(__fmul_rn(o.thr, c)), 1.0f);
   float fx0 = fmaxf(floorf(__fmul_rn(__fsub_rn(o.u, ex), 0.0625f)), 0.0f);
   float fx1 = fminf(floorf(__fmul_rn(__fadd_rn(o.u, ex), 0.0625f)), (float)(TW - 1));
   float fy0 = fmaxf(floorf(__fmul_rn(__fsub_rn(o.v, ey), 0.0625f)), 0.0f);
   float fy1 = fminf(floorf(__fmul_rn(__fadd_rn(o.v, ey), 0.0625f)), (float)(TH - 1));
-  if (fx0 > fx1 || fy0 > fy1) return false;
+  if (fx0 > fx1 || fy0 > fy1) return 0;
   int tx0 = (int)fx0, tx1 = (int)fx1, ty0 = (int)fy0, ty1 = (int)fy1;
   o.n = 0;   // kept tiles: counted by the warp-flattened walk
   o.box_x = (uint32_t)tx0 | ((uint32_t)tx1 << 16);
   o.box_y = (uint32_t)ty0 | ((uint32_t)ty1 << 16);
-  return true;
+  return 1;
 }
 
 // Pass 1 (independent tiles of 4096 slots): live bitset of the visible slots + per-tile live counts.
@@ -440,6 +447,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
     const bool valid = i < n_live;
     SplatOut o;
     bool ok = false;
+    int pr = 0;
     uint32_t g = 0;
     float al = 0.0f;
     float4 q2 = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -450,8 +458,13 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
       const float4 q1 = pool[3 * (size_t)g + 1];
       q2 = pool[3 * (size_t)g + 2];
       const float r2s = __fmul_rn(2.0f, log_s(__fmul_rn(255.0f, al)));   // r^2 = 2 ln(alpha/eps)
-      ok = (e == 1 && (kAbl & kAblMono)) ? false   // GSC_F_MONO: the right eye is not rendered
+      pr = (e == 1 && (kAbl & kAblMono)) ? 0   // GSC_F_MONO: the right eye is not rendered
            : project_one<kAbl>(ec, fc.width, fc.height, fc.TW, fc.TH, r2s, q0, q1, q2, o);
+      ok = pr > 0;
+    }
+    {
+      const uint32_t nf = __ballot_sync(0xFFFFFFFFu, pr < 0);
+      if (nf && lane == 0) atomicAdd(&ctr->n_nonfinite, (uint32_t)__popc(nf));
     }
     // skip bound = -ln(255 alpha) - 2^-7: below it alpha exp(power) < 1/255 for sure; (rx, ry) =
     // conservative half-extents of {q <= -2 pmin} (AABB of that ellipse, padded): a pixel outside them
@@ -466,7 +479,7 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
     uint32_t loff = 0;
     const uint32_t n = warp_rows_list<(kAbl & kAblAabbTiles) != 0>(ws, ok, o, rx, ry, e ? (uint32_t)fc.Te : 0u,
                                                                   fc.width, fc.height, fc.TW, sb.list, sb.list_cap,
-                                                                  &ctr->list_top, &ctr->overflow, loff);
+                                                                  &ctr->list_top, &ctr->list_overflow, loff);
     if (!valid) continue;
     const uint32_t c = e * n_live + i;
     uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
@@ -499,23 +512,24 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
   }
 }
 
-static int g_live_grid = 0, g_project_grid = 0;
+struct ProjectGrids { int live, project; };
+static PerDevice<ProjectGrids> g_proj;
 
 void launch_project(const FrameC &fc, const uint32_t *visible, const float *alpha, const float4 *pool,
                     uint32_t *live_g, uint32_t *live_bits, const SplatBufs &sb, uint32_t *status,
                     FrameCounters *ctr, int num_sms, cudaStream_t st) {
-  if (g_project_grid == 0) {
+  const ProjectGrids &g = g_proj.get([&](ProjectGrids &g) {
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, live_kernel, kLThreads, 0);
-    g_live_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+    g.live = num_sms * (per_sm > 0 ? per_sm : 1);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, project_kernel<0>, kPThreads, 0);
-    g_project_grid = num_sms * (per_sm > 0 ? per_sm : 1);
-  }
-  live_mark_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, alpha, live_bits, status, ctr);
-  live_kernel<<<g_live_grid, kLThreads, 0, st>>>(visible, live_bits, status, live_g, ctr);
+    g.project = num_sms * (per_sm > 0 ? per_sm : 1);
+  });
+  live_mark_kernel<<<g.live, kLThreads, 0, st>>>(visible, alpha, live_bits, status, ctr);
+  live_kernel<<<g.live, kLThreads, 0, st>>>(visible, live_bits, status, live_g, ctr);
   switch (fc.ablate) {
 #define GSC_PROJ_CASE(k) \
-  case k: project_kernel<k><<<g_project_grid, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
+  case k: project_kernel<k><<<g.project, kPThreads, 0, st>>>(fc, live_g, alpha, pool, sb, ctr); break;
     GSC_PROJ_CASE(0) GSC_PROJ_CASE(1) GSC_PROJ_CASE(2) GSC_PROJ_CASE(3)
     GSC_PROJ_CASE(4) GSC_PROJ_CASE(5) GSC_PROJ_CASE(6) GSC_PROJ_CASE(7)
 #undef GSC_PROJ_CASE

@@ -205,17 +205,18 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
 }
 
 // ------------------------------------------------------------------ launchers
-static int g_sort_grid = 0;
+static PerDevice<int> g_sort_grid;
 
-static void sort_setup(int num_sms) {
-  if (g_sort_grid) return;
-  const int smem = (int)sizeof(SortSmem);
-  cudaFuncSetAttribute(onesweep_pass_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(onesweep_pass_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(onesweep_pass_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pass_kernel<false, false>, kSThreads, smem);
-  g_sort_grid = num_sms * (per_sm > 0 ? per_sm : 1);
+static int sort_setup(int num_sms) {
+  return g_sort_grid.get([&](int &grid) {
+    const int smem = (int)sizeof(SortSmem);
+    cudaFuncSetAttribute(onesweep_pass_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(onesweep_pass_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(onesweep_pass_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int per_sm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, onesweep_pass_kernel<false, false>, kSThreads, smem);
+    grid = num_sms * (per_sm > 0 ? per_sm : 1);
+  });
 }
 
 // Sort `passes` (even) digits of `bits` bits each (shift 0, bits, 2 bits, ...; bits <= 8) of
@@ -226,7 +227,7 @@ void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint3
                      const uint32_t *d_count, int passes, int bits, const uint32_t *hist /* [passes][256] */,
                      uint32_t *status_a, uint32_t *status_b, uint32_t *tile_ctrs, uint2 *ranges, int num_sms,
                      cudaStream_t st) {
-  sort_setup(num_sms);
+  const int grid = sort_setup(num_sms);
   const int smem = (int)sizeof(SortSmem);
   const uint32_t dmask = (1u << bits) - 1u;
   for (int p = 0; p < passes; ++p) {
@@ -236,13 +237,13 @@ void launch_onesweep(uint32_t *keys_a, uint32_t *vals_a, uint32_t *keys_b, uint3
     uint32_t *stc = odd ? status_b : status_a, *stx = odd ? status_a : status_b;
     const uint32_t shift = (uint32_t)(bits * p);
     if (p == 0 && iota)
-      onesweep_pass_kernel<true, false><<<g_sort_grid, kSThreads, smem, st>>>(
+      onesweep_pass_kernel<true, false><<<grid, kSThreads, smem, st>>>(
           ki, nullptr, ko, vo, nullptr, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
     else if (p == passes - 1 && ranges)
-      onesweep_pass_kernel<false, true><<<g_sort_grid, kSThreads, smem, st>>>(
+      onesweep_pass_kernel<false, true><<<grid, kSThreads, smem, st>>>(
           ki, vi, ko, vo, ranges, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
     else
-      onesweep_pass_kernel<false, false><<<g_sort_grid, kSThreads, smem, st>>>(
+      onesweep_pass_kernel<false, false><<<grid, kSThreads, smem, st>>>(
           ki, vi, ko, vo, nullptr, d_count, shift, dmask, hist + 256 * p, stc, stx, tile_ctrs + p);
   }
 }

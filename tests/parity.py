@@ -4,12 +4,19 @@ The bar (BASELINE.json north_star): visible-anchor sets, cache hit/miss sets
 and sorted key order bit-exact; pixels within 2e-3 absolute per RGB channel
 in fp32 with PSNR >= 55 dB.  Derived Gaussians, splat records and sorted keys
 are compared bit for bit as well (DESIGN.md Numerics: both sides execute the
-same IEEE op sequence).
+same IEEE op sequence up to the blend's exponential, R5).
 """
 import numpy as np
 
 PIX_TOL = 2e-3
 PSNR_MIN = 55.0
+# The blend's exponential runs on the SFU (ex2.approx, SURVEY §8c-4 R5).  Pixels where a skip or stop
+# decision could differ from the oracle's (alpha' within 2^-19 of 1/255, power > 0, T' within the
+# error band of 1e-4 with a contribution > 1e-4 at stake) are replayed exactly (blend.cu), so a pixel
+# differs from the oracle only by (a) its contributions' rounding -- relative error of T and of every
+# weight <= 5e-4 in the worst case, ~1e-6 in practice -- and (b) an unreplayed stop flip, which moves
+# it by at most kJump = 1e-4.  Bound: 1e-4 + 5e-4 (x |C| <= 1) -- inside north_star's 2e-3 / 55 dB.
+BLEND_FAST_TOL = 6e-4
 
 
 def psnr(a, b):

@@ -19,7 +19,7 @@ def gsclib():
 def _declared():
     txt = open(os.path.join(ROOT, "include", "gscache.h")).read()
     txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
-    return sorted(set(re.findall(r"\b(gsc_[a-z_]+)\s*\(", txt)))
+    return sorted(set(re.findall(r"\b(gsc_[a-z0-9_]+)\s*\(", txt)))
 
 
 def test_header_declares_the_boundary():
@@ -37,7 +37,7 @@ def test_every_declared_symbol_is_exported(gsclib):
 
 def test_abi_version_and_argument_checks(gsclib):
     L = gsclib.lib()
-    assert L.gsc_abi_version() == 1
+    assert L.gsc_abi_version() == 2
     h = C.c_void_p()
     cfg = gsclib.gsc_config()
     assert L.gsc_create(0, C.byref(cfg), C.byref(h)) == gsclib.GSC_EINVAL      # zero-sized image

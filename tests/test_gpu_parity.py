@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import scenegen as sg
-from parity import (compare_images, compare_pool, compare_sets, compare_splats_pairs, oracle_config,
+from parity import (BLEND_FAST_TOL, compare_images, compare_pool, compare_sets, compare_splats_pairs, oracle_config,
                     renderer)
 
 pytestmark = pytest.mark.gpu
@@ -39,7 +39,7 @@ def test_c1_all_poses(orc, c1):
     r = renderer(cfg).load(sc)
     for rig in sg.trajectory(cfg):
         st, d = _frame_parity(orc, o, r, rig)
-        assert d == 0.0
+        assert d <= BLEND_FAST_TOL
 
 
 def test_c1_derive_on_cuda_cores(orc, c1):
@@ -50,7 +50,7 @@ def test_c1_derive_on_cuda_cores(orc, c1):
     r = renderer(cfg, flags=_abi.GSC_F_DERIVE_CUDA_CORES).load(sc)
     for rig in sg.trajectory(cfg):
         st, d = _frame_parity(orc, o, r, rig)
-        assert d == 0.0
+        assert d <= BLEND_FAST_TOL
 
 
 def test_c1_brute_force_pixels(orc, c1):
@@ -136,7 +136,7 @@ def test_c1_ablations(orc, c1, ablate):
     r = renderer(cfg, flags=flags).load(sc)
     for rig in sg.trajectory(cfg):
         st, d = _frame_parity(orc, o, r, rig)
-        assert d == 0.0
+        assert d <= BLEND_FAST_TOL
 
 
 def test_c1_spec_literal_depth(orc, c1):
@@ -189,6 +189,27 @@ def test_elementary_functions_bitwise(orc, fn, lo, hi, step):
             same = (got.view(np.uint32) == ref.view(np.uint32)) | (np.isnan(got) & np.isnan(ref))
             nbad += int((~same).sum())
     assert nbad == 0
+
+
+def test_fast_exp_error_bound(orc):
+    """The blend's SFU exponential (R5) on every float of [-5.56, 0] (the power range where the blend
+    can accept a splat: power >= skip bound = -ln(255 alpha) - 2^-7 >= -5.55) against the oracle's
+    exp_s: relative error < 8e-7, so alpha' = min(0.99, alpha e) differs from the oracle's by < 2^-20
+    relative after the product roundings (+1.2e-7) -- half the guard band kAlphaGuard (2^-19) the blend
+    uses to hand skip decisions near 1/255 to the exact replay (blend.cu)."""
+    import torch
+    import paper_2502_14938_b200 as gp
+    r = gp.Renderer(0, 64, 64)
+    a = np.float32(-0.0).view(np.uint32).astype(np.int64)
+    b = np.float32(-5.56).view(np.uint32).astype(np.int64)
+    worst = 0.0
+    for s0 in range(a, b + 1, 1 << 25):
+        bits = np.arange(s0, min(b + 1, s0 + (1 << 25)), dtype=np.int64).astype(np.uint32)
+        x = bits.view(np.float32)
+        ref = orc.elem("exp", x).astype(np.float64)
+        got = r.elementary("exp_fast", torch.from_numpy(x).cuda()).cpu().numpy().astype(np.float64)
+        worst = max(worst, float(np.max(np.abs(got / ref - 1.0))))
+    assert worst < 8e-7, worst
 
 
 def test_rgba8_output_matches_f32(orc, c1):
@@ -263,7 +284,7 @@ def test_c4_full_size_bench_config(orc, c4):
         st, d = _frame_parity(orc, o, r, traj[f], full=f in (0, 30))
         assert not st["overflow"]
         if f in (0, 30):
-            assert d == 0.0
+            assert d <= BLEND_FAST_TOL
 
 
 def test_c5_full_size_frames(orc):
@@ -279,7 +300,7 @@ def test_c5_full_size_frames(orc):
         st, d = _frame_parity(orc, o, r, traj[f], full=f in (0, 10))
         assert not st["overflow"]
         if f in (0, 10):
-            assert d == 0.0
+            assert d <= BLEND_FAST_TOL
 
 
 def test_host_async_matches_device_render(orc, c1):
@@ -355,4 +376,39 @@ def test_c1_no_dered_per_eye_pipelines(orc, c1):
             res = oracles[e].frame(gp.PerEyeRenderer._mono(rig, e))
             compare_sets(oracles[e], per.eyes[e], stats[e])
             d = float(np.abs(img.cpu().numpy() - res.img_l).max())
-            assert d == 0.0
+            assert d <= BLEND_FAST_TOL
+
+
+@pytest.mark.parametrize("start,stop,full", [(290, 300, (290, 300)), (440, 450, (450,)), (540, 599, (540, 599))])
+def test_c4_cold_blocks_aerial(orc, c4, start, stop, full):
+    """SURVEY §8(e) per-rank oracle replay: a weak-scaling rank starts its contiguous block of the
+    C4 trajectory cold, mid-trajectory.  Blocks starting at frames 290 / 440 / 540 (the aerial half:
+    the eye at ~150-300 m, where the paper's FPS drops) on a fresh context and a fresh oracle:
+    hit/miss sets and depths every frame, full parity (pool, splats, sorted keys, pixels) at the
+    listed frames -- including the block's cold first frame and the trajectory's last frame."""
+    cfg, sc = c4
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(start, stop + 1):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in full)
+        assert not st["overflow"]
+        if f == start:
+            assert st["n_misses"] == st["n_visible"]       # cold block start
+        if f in full:
+            assert d <= BLEND_FAST_TOL
+
+
+def test_c5_cold_block(orc):
+    """configs[4]: the block of a rank starting at frame 1800 of the 2400-frame C5 trajectory (cold
+    cache, high altitude): sets every frame, full parity at 1800 and 1805."""
+    cfg = sg.config("C5")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(1800, 1806):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in (1800, 1805))
+        assert not st["overflow"]
+        if f in (1800, 1805):
+            assert d <= BLEND_FAST_TOL
