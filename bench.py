@@ -135,7 +135,7 @@ def run_gsc(args):
     traj = sg.trajectory(cfg)
     fmt = gp.GSC_FMT_RGBA8
     free0 = torch.cuda.mem_get_info(dev)[0]
-    base = gp.GSC_F_STAGGER if args.stagger else 0   # the F3 variant (R26); 0 = the method
+    base = (gp.GSC_F_STAGGER if args.stagger else 0) | (gp.GSC_F_BLEND_EXACT if args.blend_exact else 0)
     r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
                     flags=base, pair_capacity=args.pair_capacity).load(sc)
     torch.cuda.synchronize()
@@ -286,7 +286,8 @@ def run_gsc(args):
                        "frames_per_rank": len(frames), "out_format": "rgba8",
                        "l2": "no flush: per-frame working set (pool/splat/pair traffic ~1-2 GB) > 126 MB L2",
                        "parallelism": f"frames partitioned by view, scene replicated, dp{world}",
-                       **({"variant": "staggered expiry (GSC_F_STAGGER, F3)"} if args.stagger else {})},
+                       **({"variant": "staggered expiry (GSC_F_STAGGER, F3)"} if args.stagger else {}),
+                       **({"blend": "exact exponential (GSC_F_BLEND_EXACT)"} if args.blend_exact else {})},
             "stages": stage_report,
             "stages_note": "CUDA events per stage in a replay of the same frames with GSC_F_SERIAL (no overlap of "
                            "frame f+1's front end with frame f's blend); the timed run overlaps them on two streams",
@@ -387,6 +388,7 @@ def main():
     ap.add_argument("--pair-capacity", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stagger", action="store_true", help="staggered expiry variant (GSC_F_STAGGER, SURVEY 8(f) F3)")
+    ap.add_argument("--blend-exact", action="store_true", help="blend with exp_s on every evaluation (GSC_F_BLEND_EXACT)")
     ap.add_argument("--cpu-sample-frames", type=int, default=1)
     ap.add_argument("--ref-frames", type=int, default=4)
     args = ap.parse_args()

@@ -87,6 +87,10 @@ typedef struct gsc_ctx gsc_ctx;
                                        first frame) expire spread over D_max frames, not all at once
                                        (no periodic full re-derivation spikes).  Applies from the next
                                        gsc_reset_cache / load */
+#define GSC_F_BLEND_EXACT 0x800u   /* blend with the exact exponential exp_s on every evaluation (pixels bit-identical
+                                       to the oracle); default: the SFU exponential with exactness guards and an
+                                       exact replay of the pixels whose decisions it could flip (
+                                       pixels within 6e-4 of the oracle, decisions identical) */
 #define GSC_F_SERIAL 0x10u       /* do not overlap frame f+1's front end (cull .. ranges) with frame f's
                                     blend: per-stage times then add up to the frame time */
 

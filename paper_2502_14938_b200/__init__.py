@@ -11,13 +11,13 @@ import math
 
 from . import _abi
 from ._abi import (GSC_F_ABL_AABB_TILES, GSC_F_ABL_FIXED_EXTENT, GSC_F_COUNT_EVALS, GSC_F_DEPTH_LITERAL,
-                   GSC_F_DERIVE_CUDA_CORES, GSC_F_GUIDE_EXP, GSC_F_MONO, GSC_F_STAGGER,
+                   GSC_F_DERIVE_CUDA_CORES, GSC_F_GUIDE_EXP, GSC_F_MONO, GSC_F_STAGGER, GSC_F_BLEND_EXACT,
                    GSC_F_GUIDE_STAGED, GSC_F_SERIAL, GSC_F_STAGE_TIMING,
                    GSC_FMT_RGB_F32_PLANAR, GSC_FMT_RGBA8, GscError, gsc_frame_stats)
 
 __all__ = ["Renderer", "GscError", "GSC_F_DEPTH_LITERAL", "GSC_F_STAGE_TIMING", "GSC_F_DERIVE_CUDA_CORES",
            "GSC_F_COUNT_EVALS", "GSC_F_SERIAL", "GSC_F_GUIDE_EXP", "GSC_F_GUIDE_STAGED", "GSC_F_ABL_FIXED_EXTENT",
-           "GSC_F_ABL_AABB_TILES", "GSC_F_MONO", "GSC_F_STAGGER", "PerEyeRenderer", "GSC_FMT_RGB_F32_PLANAR",
+           "GSC_F_ABL_AABB_TILES", "GSC_F_MONO", "GSC_F_STAGGER", "GSC_F_BLEND_EXACT", "PerEyeRenderer", "GSC_FMT_RGB_F32_PLANAR",
            "GSC_FMT_RGBA8", "build"]
 
 

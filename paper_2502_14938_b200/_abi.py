@@ -28,6 +28,7 @@ GSC_F_ABL_FIXED_EXTENT = 0x80
 GSC_F_ABL_AABB_TILES = 0x100
 GSC_F_MONO = 0x200
 GSC_F_STAGGER = 0x400
+GSC_F_BLEND_EXACT = 0x800
 GSC_FMT_RGB_F32_PLANAR = 0
 GSC_FMT_RGBA8 = 1
 DBG = {"visible": 1, "misses": 2, "pool": 3, "splats": 4, "splat_g": 5, "pairs": 6, "pair_g": 7, "ranges": 8,

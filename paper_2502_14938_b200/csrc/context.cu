@@ -36,7 +36,7 @@ void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, int,
                  cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
-                  const float4 *, void *, void *, int, FrameCounters *, uint32_t *, bool, int, cudaStream_t);
+                  const float4 *, void *, void *, int, FrameCounters *, uint32_t *, bool, bool, int, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 void launch_derive_f32(const float pu[3], const uint32_t *, const float4 *, const float *, const float *, const float *,
                        const float *, const float *, const float *, const float *, float *, float4 *, FrameCounters *,
@@ -613,7 +613,7 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   CU(cudaStreamWaitEvent(sB, ctx->ev_user[k], 0));
   mark(sB);
   launch_blend(fc, S.ranges.p, S.pkey.p, S.pval.p, S.spA.p, S.spB.p, S.spC.p, out_l, out_r, fmt, ctr, ctx->fixup.p,
-               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, ctx->num_sms, sB);
+               (ctx->cfg.flags & GSC_F_COUNT_EVALS) != 0, (ctx->cfg.flags & GSC_F_BLEND_EXACT) != 0, ctx->num_sms, sB);
   launch_record(ctr, ctx->rec_dev.p + slot_i, sB);
   CU(cudaMemcpyAsync(ctx->rec_host + slot_i, ctx->rec_dev.p + slot_i, sizeof(FrameRecordDev), cudaMemcpyDeviceToHost,
                      sB));
@@ -810,7 +810,8 @@ gsc_status gsc_set_flags(gsc_ctx *ctx, unsigned flags) {
   if (!ctx) return GSC_EINVAL;
   const unsigned known =
       GSC_F_DEPTH_LITERAL | GSC_F_STAGE_TIMING | GSC_F_DERIVE_CUDA_CORES | GSC_F_COUNT_EVALS | GSC_F_SERIAL |
-      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES | GSC_F_MONO | GSC_F_STAGGER;
+      GSC_F_GUIDE_EXP | GSC_F_GUIDE_STAGED | GSC_F_ABL_FIXED_EXTENT | GSC_F_ABL_AABB_TILES | GSC_F_MONO | GSC_F_STAGGER |
+      GSC_F_BLEND_EXACT;
   if (flags & ~known) return fail(ctx, GSC_EINVAL, "unknown flag bits");
   if ((flags & GSC_F_GUIDE_EXP) && (flags & GSC_F_GUIDE_STAGED)) return fail(ctx, GSC_EINVAL, "two guiding functions");
   CU(cudaSetDevice(ctx->device));

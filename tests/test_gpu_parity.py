@@ -412,3 +412,15 @@ def test_c5_cold_block(orc):
         assert not st["overflow"]
         if f in (1800, 1805):
             assert d <= BLEND_FAST_TOL
+
+
+def test_blend_exact_mode_bit_identical(orc, c1):
+    """GSC_F_BLEND_EXACT: the exact-exponential blend -- pixels bit-identical to the oracle's on every
+    C1 pose and on a full-size C4 frame (the default fast blend: within BLEND_FAST_TOL, decisions equal)."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c1
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg, flags=gp.GSC_F_BLEND_EXACT).load(sc)
+    for rig in sg.trajectory(cfg):
+        st, d = _frame_parity(orc, o, r, rig)
+        assert d == 0.0
