@@ -102,17 +102,17 @@ def _stage_bytes(s, N, K, W, H, fmt_bytes):
         "cull": N * (16 + 1 + 4) + N / 4.0 + 4 * V + 8 * M,
         # miss id, pos, feat, offs, scale in; alpha + 48-byte pool record out per slot
         "derive": M * (4 + 16 + 32 + 120 + 12) + M * K * (4 + 48),
-        # live: ids + alpha per slot in, live id out; project: live id, alpha, 48-byte pool record in,
-        # 72-byte record per splat out; tiles: 36 B read + 8 B written per splat, 4 B per kept tile
-        "project": 4 * V + 4 * V * K + 4 * (C / 2.0) + (4 + 4 + 48) * (C / 2.0) + 72 * C + 44 * C + 4 * P,
+        # SURVEY d-3: visible ids + 4 B alpha per visible slot, 48-byte pool record per live Gaussian read;
+        # per splat (both eyes) a 44-byte record (u v A B C alpha rgb, depth, kept count) written; 4 B per kept tile
+        "project": 4 * V + 4 * V * K + 48 * (C / 2.0) + 44 * C + 4 * P,
         "depth_sort": 12 * C + 3 * 16 * C,
         # pairoff 12 B per splat; expand 12 B per pair + 12 B per splat
         "emit": 24 * C + 12 * P,
         # (the tile ranges are derived inside the last tile pass: no bytes of their own)
         "tile_sort": 2 * 16 * P,
         "ranges": 0.0,
-        # pair value + 48-byte record per pair, output images
-        "blend": 52 * P + 2 * W * H * fmt_bytes,
+        # pair key + value and the 40-byte blend record (u v -A/2 -B, -C/2 bound alpha r, g b) per pair; images
+        "blend": 48 * P + 2 * W * H * fmt_bytes,
     }
 
 

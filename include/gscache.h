@@ -169,7 +169,7 @@ typedef struct {
 #define GSC_DBG_VISIBLE 1     /* uint32 anchor ids of X_f, ascending */
 #define GSC_DBG_MISSES 2      /* uint32 anchor ids decoded this frame, ascending */
 #define GSC_DBG_POOL 3        /* float [N*10][13]: alpha, mu[3], cov[6] (00 01 02 11 12 22), rgb[3] by slot g=i*10+j */
-#define GSC_DBG_SPLATS 4      /* float [n_splats][13]: u v A B C alpha r g b depth thr eye kept_tiles; compaction order
+#define GSC_DBG_SPLATS 4      /* float [n_splats][13]: u v A B C alpha r g b depth thr(NaN: not kept) eye kept_tiles; compaction order
                                  (per warp tile: eye-major, slot ascending); includes boxes with 0 kept tiles */
 #define GSC_DBG_SPLAT_G 5     /* uint32 [n_splats]: Gaussian slot g of each splat (same order) */
 #define GSC_DBG_PAIRS 6       /* uint64 [n_pairs]: sorted (tile << 32 | depth bits), tile = eye*T_e + ty*TW + tx */

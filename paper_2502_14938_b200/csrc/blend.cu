@@ -92,7 +92,7 @@ template <bool kCount>   // kCount: accumulate n_evals / n_exp (GSC_F_COUNT_EVAL
 __global__ void __launch_bounds__(kBThreads)
 blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
              const uint32_t *__restrict__ pair_vals,
-             const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
+             const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float2 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr,
              uint32_t *__restrict__ fixup) {
   // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
@@ -140,7 +140,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
       const uint32_t slot = __popc(bits & lt);
       slots[warp][slot] = spA[c];
       slots[warp][32 + slot] = spB[c];
-      slots[warp][64 + slot] = spC[c];
+      *reinterpret_cast<float2 *>(&slots[warp][64 + slot]) = spC[c];
     }
     const uint32_t n = __popc(bits);
     __syncwarp();
@@ -216,7 +216,7 @@ template <bool kCount>
 __global__ void __launch_bounds__(kBThreads)
 blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
              const uint32_t *__restrict__ pair_vals,
-             const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float4 *__restrict__ spC,
+             const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float2 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr) {
   // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
   // walks all three (offsets 0, 512, 1024 bytes)
@@ -260,7 +260,7 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
       const uint32_t slot = __popc(bits & lt);
       slots[warp][slot] = spA[c];
       slots[warp][32 + slot] = spB[c];
-      slots[warp][64 + slot] = spC[c];
+      *reinterpret_cast<float2 *>(&slots[warp][64 + slot]) = spC[c];
     }
     const uint32_t n = __popc(bits);
     __syncwarp();
@@ -320,7 +320,7 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
 __global__ void __launch_bounds__(128)
 blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
                    const uint32_t *__restrict__ pair_vals, const float4 *__restrict__ spA,
-                   const float4 *__restrict__ spB, const float4 *__restrict__ spC, void *__restrict__ out_l,
+                   const float4 *__restrict__ spB, const float2 *__restrict__ spC, void *__restrict__ out_l,
                    void *__restrict__ out_r, int fmt, const FrameCounters *__restrict__ ctr,
                    const uint32_t *__restrict__ fixup) {
   const uint32_t lane = lane_id();
@@ -344,7 +344,8 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
       float al = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
       if (i < r1 && (pair_keys[i] & wbit)) {
         const uint32_t c = pair_vals[i];
-        const float4 a = spA[c], q = spB[c], cc = spC[c];
+        const float4 a = spA[c], q = spB[c];
+        const float2 cc = spC[c];
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
         const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
@@ -373,7 +374,7 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
 }
 
 void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_keys, const uint32_t *pair_vals,
-                  const float4 *spA, const float4 *spB, const float4 *spC, void *out_l, void *out_r, int fmt,
+                  const float4 *spA, const float4 *spB, const float2 *spC, void *out_l, void *out_r, int fmt,
                   FrameCounters *ctr, uint32_t *fixup, bool count, bool exact, int num_sms, cudaStream_t st) {
   const int grid = (fc.ablate & kAblMono) ? fc.Te : 2 * fc.Te;   // GSC_F_MONO: left eye tiles only
   if (exact) {

@@ -36,7 +36,7 @@ void launch_onesweep(uint32_t *, uint32_t *, uint32_t *, uint32_t *, bool, const
 void launch_emit(const EmitIn &, uint32_t, uint32_t *, uint32_t *, uint32_t *, FrameCounters *, int, int,
                  cudaStream_t);
 void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_t *, const float4 *, const float4 *,
-                  const float4 *, void *, void *, int, FrameCounters *, uint32_t *, bool, bool, int, cudaStream_t);
+                  const float2 *, void *, void *, int, FrameCounters *, uint32_t *, bool, bool, int, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 void launch_derive_f32(const float pu[3], const uint32_t *, const float4 *, const float *, const float *, const float *,
                        const float *, const float *, const float *, const float *, float *, float4 *, FrameCounters *,
@@ -104,7 +104,8 @@ struct gsc_ctx {
   // What the blend of frame f reads lives in fs[f & 1]: the next frame's front end (cull .. ranges,
   // stream sA) runs while this frame's blend (stream sB) still reads its set (inter-frame pipeline).
   struct FrameSet {
-    DevBuf<float4> spA, spB, spC;
+    DevBuf<float4> spA, spB;
+    DevBuf<float2> spC;
     DevBuf<uint32_t> pkey, pval;           // tile-sorted pairs
     DevBuf<uint2> ranges;
     DevBuf<unsigned char> zero_region;     // FrameCounters | cull status | project status | emit status
@@ -113,9 +114,7 @@ struct gsc_ctx {
   cudaStream_t sA = nullptr, sB = nullptr;
   cudaEvent_t ev_user[2] = {nullptr, nullptr}, ev_a[2] = {nullptr, nullptr}, ev_b[2] = {nullptr, nullptr};
   bool b_pending[2] = {false, false};
-  DevBuf<float2> spD;
-  DevBuf<uint2> box;
-  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, gslot, list_off, pair_off, list, live_g;
+  DevBuf<uint32_t> count, dkey_a, dval_a, dkey_b, dval_b, list_off, pair_off, list, live_g;
   DevBuf<uint32_t> live_bits;   // live bitset of the visible slots (live_mark -> live)
   DevBuf<uint32_t> pkey_b, pval_b;         // tile-sort scratch (front end only)
   DevBuf<uint32_t> fixup;                  // blend: pixels for the exact replay (blends run in frame order)
@@ -369,10 +368,7 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *g, const gsc_
     CU(S.spB.alloc(ctx->cap_splat));
     CU(S.spC.alloc(ctx->cap_splat));
   }
-  CU(ctx->spD.alloc(ctx->cap_splat));
-  CU(ctx->box.alloc(ctx->cap_splat));
   CU(ctx->count.alloc(ctx->cap_splat));
-  CU(ctx->gslot.alloc(ctx->cap_splat));
   CU(ctx->live_g.alloc(ctx->cap_splat / 2));
   CU(ctx->live_bits.alloc(ctx->cap_splat / 64 + 1));
   CU(ctx->dkey_a.alloc(ctx->cap_splat));
@@ -584,8 +580,8 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
                   (ctx->cfg.flags & GSC_F_DERIVE_CUDA_CORES) == 0, sA);
   mark(sA);
   // a4
-  SplatBufs sb{S.spA.p, S.spB.p, S.spC.p, ctx->spD.p, ctx->box.p, ctx->count.p, ctx->dkey_a.p, ctx->gslot.p,
-               ctx->list_off.p, ctx->list.p, (uint32_t)ctx->list.n};
+  SplatBufs sb{S.spA.p, S.spB.p, S.spC.p, ctx->count.p, ctx->dkey_a.p, ctx->list_off.p, ctx->list.p,
+               (uint32_t)ctx->list.n};
   launch_project(fc, ctx->visible.p, ctx->alpha.p, ctx->pool.p, ctx->live_g.p, ctx->live_bits.p, sb,
                  reinterpret_cast<uint32_t *>(S.zero_region.p + ctx->off_proj), ctr, ctx->num_sms, sA);
   mark(sA);
@@ -829,25 +825,52 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
   FrameCounters c;
   CU(cudaMemcpy(&c, S.zero_region.p, sizeof(c), cudaMemcpyDeviceToHost));
   const size_t NK = (size_t)ctx->N * kK;
-  const size_t ns = c.n_splat, np = c.n_pairs;
+  const size_t ns = c.n_splat, np = c.n_pairs, nlive = ns / 2;
   auto copy_dev = [&](const void *src, size_t bytes) -> gsc_status {
     *len = bytes;
     if (host_dst && cap) CU(cudaMemcpy(host_dst, src, std::min(cap, bytes), cudaMemcpyDeviceToHost));
+    return GSC_OK;
+  };
+  // splat c = eye * n_live + i is live Gaussian live_g[i] (project.cu); its depth key sits in the
+  // depth-sorted (key, splat) arrays of the frame's depth sort
+  std::vector<uint32_t> gof, dof;
+  auto load_g = [&]() -> gsc_status {
+    std::vector<uint32_t> lg(nlive);
+    if (nlive) CU(cudaMemcpy(lg.data(), ctx->live_g.p, nlive * 4, cudaMemcpyDeviceToHost));
+    gof.resize(ns);
+    for (size_t k = 0; k < ns; ++k) gof[k] = lg[k % nlive];
+    return GSC_OK;
+  };
+  auto load_depth = [&]() -> gsc_status {
+    std::vector<uint32_t> dk(ns), dv(ns);
+    if (ns) {
+      CU(cudaMemcpy(dk.data(), ctx->dkey_a.p, ns * 4, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(dv.data(), ctx->dval_a.p, ns * 4, cudaMemcpyDeviceToHost));
+    }
+    dof.assign(ns, 0xFFFFFFFFu);
+    for (size_t k = 0; k < ns; ++k)
+      if (dv[k] < ns) dof[dv[k]] = dk[k];
     return GSC_OK;
   };
   switch (what) {
     case GSC_DBG_VISIBLE: return copy_dev(ctx->visible.p, (size_t)c.n_visible * 4);
     case GSC_DBG_MISSES: return copy_dev(ctx->misses.p, (size_t)c.n_miss * 4);
     case GSC_DBG_BIRTH: return copy_dev(ctx->birth.p, (size_t)ctx->N * 4);
-    case GSC_DBG_SPLAT_G: return copy_dev(ctx->gslot.p, ns * 4);
+    case GSC_DBG_SPLAT_G: {
+      *len = ns * 4;
+      if (!host_dst || !cap) return GSC_OK;
+      if (load_g() != GSC_OK) return GSC_ECUDA;
+      std::memcpy(host_dst, gof.data(), std::min(cap, ns * 4));
+      return GSC_OK;
+    }
     case GSC_DBG_PAIR_G: {
       *len = np * 4;
       if (!host_dst || !cap) return GSC_OK;
-      std::vector<uint32_t> pv(np), gs(ns);
+      std::vector<uint32_t> pv(np);
       CU(cudaMemcpy(pv.data(), S.pval.p, np * 4, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(gs.data(), ctx->gslot.p, ns * 4, cudaMemcpyDeviceToHost));
+      if (load_g() != GSC_OK) return GSC_ECUDA;
       std::vector<uint32_t> out(np);
-      for (size_t k = 0; k < np; ++k) out[k] = gs[pv[k]];
+      for (size_t k = 0; k < np; ++k) out[k] = gof[pv[k]];
       std::memcpy(host_dst, out.data(), std::min(cap, np * 4));
       return GSC_OK;
     }
@@ -855,16 +878,12 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
       *len = np * 8;
       if (!host_dst || !cap) return GSC_OK;
       std::vector<uint32_t> pk(np), pv(np);
-      std::vector<float2> D(ns);
       CU(cudaMemcpy(pk.data(), S.pkey.p, np * 4, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(pv.data(), S.pval.p, np * 4, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
+      if (load_depth() != GSC_OK) return GSC_ECUDA;
       std::vector<uint64_t> out(np);
-      for (size_t k = 0; k < np; ++k) {
-        uint32_t db;
-        std::memcpy(&db, &D[pv[k]].y, 4);
-        out[k] = ((uint64_t)(pk[k] & 0x00FFFFFFu) << 32) | db;   // bits 24..31: blend block mask
-      }
+      for (size_t k = 0; k < np; ++k)
+        out[k] = ((uint64_t)(pk[k] & 0x00FFFFFFu) << 32) | dof[pv[k]];   // bits 24..31: blend block mask
       std::memcpy(host_dst, out.data(), std::min(cap, np * 8));
       return GSC_OK;
     }
@@ -896,22 +915,23 @@ gsc_status gsc_debug_fetch(gsc_ctx *ctx, int what, void *host_dst, size_t cap, s
     case GSC_DBG_SPLATS: {
       *len = ns * 13 * 4;
       if (!host_dst || !cap) return GSC_OK;
-      std::vector<float4> A(ns), B(ns), Cc(ns);
-      std::vector<float2> D(ns);
-      std::vector<uint2> bx(ns);
+      std::vector<float4> A(ns), B(ns);
+      std::vector<float2> Cc(ns);
       std::vector<uint32_t> cn(ns);
       CU(cudaMemcpy(A.data(), S.spA.p, ns * 16, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(B.data(), S.spB.p, ns * 16, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(Cc.data(), S.spC.p, ns * 16, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(D.data(), ctx->spD.p, ns * 8, cudaMemcpyDeviceToHost));
-      CU(cudaMemcpy(bx.data(), ctx->box.p, ns * 8, cudaMemcpyDeviceToHost));
+      CU(cudaMemcpy(Cc.data(), S.spC.p, ns * 8, cudaMemcpyDeviceToHost));
       CU(cudaMemcpy(cn.data(), ctx->count.p, ns * 4, cudaMemcpyDeviceToHost));
+      if (load_depth() != GSC_OK) return GSC_ECUDA;
       std::vector<float> out(ns * 13);
+      const float nan = std::nanf("");
       for (size_t k = 0; k < ns; ++k) {
-        // records hold (u, v, -A/2, -B), (-C/2, bound, alpha, r), (g, b, rx, ry), (thr, depth);
-        // -2 x (-A/2) is exact
+        // records hold (u, v, -A/2, -B), (-C/2, bound, alpha, r), (g, b); -2 x (-A/2) is exact.  thr is not
+        // kept per splat (NaN here); the kept-tile count and the sorted keys it decides are.
+        float depth;
+        std::memcpy(&depth, &dof[k], 4);
         float r[13] = {A[k].x, A[k].y, -2.0f * A[k].z, -A[k].w, -2.0f * B[k].x, B[k].z, B[k].w, Cc[k].x, Cc[k].y,
-                       D[k].y, D[k].x, (float)(bx[k].y >> 31), (float)cn[k]};
+                       depth, nan, (float)(k >= nlive), (float)cn[k]};
         std::memcpy(&out[13 * k], r, sizeof(r));
       }
       std::memcpy(host_dst, out.data(), std::min(cap, out.size() * 4));

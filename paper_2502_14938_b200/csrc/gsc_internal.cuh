@@ -74,12 +74,9 @@ struct PolicyState {
 struct SplatBufs {
   float4 *spA;       // (u, v, -A/2, -B)     A,B,C = conic (A dx^2 + 2B dx dy + C dy^2)
   float4 *spB;       // (-C/2, skip bound, alpha, r)
-  float4 *spC;       // (g, b, rx, ry): colour and the half-extents of {power >= skip bound} (blend strip cull)
-  float2 *spD;       // (thr, depth)
-  uint2 *box;        // candidate tile box: tx0 | tx1 << 16 ; ty0 | ty1 << 16 | eye << 31
+  float2 *spC;       // (g, b): the rest of the colour
   uint32_t *count;   // kept tiles
   uint32_t *depth;   // depth key = bits(z) (depth-sort input)
-  uint32_t *gslot;   // Gaussian slot g
   uint32_t *list_off;  // start of the splat's kept-tile keys in `list`
   uint32_t *list;      // kept-tile keys (eye*T_e + ty*TW + tx), per splat contiguous, row-major
   uint32_t list_cap;

@@ -484,18 +484,13 @@ project_kernel(FrameC fc, const uint32_t *__restrict__ live_g, const float *__re
     const uint32_t c = e * n_live + i;
     uint32_t dk = 0xFFFFFFFFu;      // a dead entry sorts last and owns no tile
     if (ok) {
-      // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b, rx, ry), (thr, depth)
+      // blend-ready record (N6): (u, v, -A/2, -B), (-C/2, skip bound, alpha, r), (g, b); 40 bytes
       dk = __float_as_uint(o.depth);
       sb.spA[c] = make_float4(o.u, o.v, __fmul_rn(-0.5f, o.A), -o.B);
       sb.spB[c] = make_float4(__fmul_rn(-0.5f, o.C), pmin, al, q2.y);
-      sb.box[c] = make_uint2(o.box_x, o.box_y | (e << 31));
-      sb.spC[c] = make_float4(q2.z, q2.w, rx, ry);
-      sb.spD[c] = make_float2(o.thr, __uint_as_float(dk));
-    } else {
-      sb.box[c] = make_uint2(0x0000FFFFu, e << 31);   // tx0 = 65535 > tx1 = 0: empty
+      sb.spC[c] = make_float2(q2.z, q2.w);
     }
     sb.depth[c] = dk;
-    sb.gslot[c] = g;
     sb.count[c] = n;
     sb.list_off[c] = loff;
     pairs_local += n;

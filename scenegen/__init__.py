@@ -36,7 +36,7 @@ import numpy as np
 
 __all__ = [
     "splitmix64", "uniform01", "Scene", "Rig", "make_city_scene",
-    "make_orbit", "look_at_rig", "write_gsc2", "read_gsc2", "with_real_weights",
+    "make_orbit", "make_pan", "look_at_rig", "write_gsc2", "read_gsc2", "with_real_weights",
     "write_trajectory", "read_trajectory", "config", "CONFIGS",
     "F_DIM", "K_GAUSS", "H_DIM",
 ]
@@ -307,6 +307,26 @@ def make_orbit(center, radius0: float, radius1: float, h0: float, h1: float,
     return rigs
 
 
+def make_pan(eye0, eye1, yaw0_deg: float, steps_deg, pitch_deg: float = -5.0, ipd: float = 0.064,
+             fps: float = 90.0):
+    """Head-turn trajectory for the F3 depth-policy study ("movement with acceleration and with
+    staged speed changes"): the eye moves linearly from eye0 to eye1 while the view direction turns
+    about the vertical by steps_deg[f] degrees at frame f (yaw speed profile), pitched by pitch_deg."""
+    e0, e1 = np.asarray(eye0, np.float64), np.asarray(eye1, np.float64)
+    n = len(steps_deg)
+    rigs = []
+    yaw = math.radians(yaw0_deg)
+    pitch = math.radians(pitch_deg)
+    for f in range(n):
+        if f:
+            yaw += math.radians(steps_deg[f])
+        a = f / max(1, n - 1)
+        eye = e0 + (e1 - e0) * a
+        d = np.array([math.cos(yaw) * math.cos(pitch), math.sin(yaw) * math.cos(pitch), math.sin(pitch)])
+        rigs.append(look_at_rig(eye, eye + d, ipd, t=f / fps))
+    return rigs
+
+
 # ----------------------------------------------------------------------------
 # files
 # ----------------------------------------------------------------------------
@@ -436,6 +456,11 @@ CONFIGS = {
     "C1R": Config("C1R", 1000, 20.0, 3, 64, 64, 70.0, 10, real=True),
     "C3R": Config("C3R", 100_000, 130.0, 5, 1920, 1080, 70.0, 10, real=True),
     "C3S": Config("C3S", 100_000, 130.0, 1, 1920, 1080, 70.0, 10, real=True),
+    # SURVEY §8(f) F3 (depth-policy study): the C3 scene with a street-level head turn whose speed
+    # accelerates (C3A: 0.2 -> 40 deg/frame over 300 frames) or changes in stages (C3T: 1 / 10 / 35 deg
+    # per frame, 100 frames each) -- the novelty rate then spans 0 -> ~30%, where the guides differ
+    "C3A": Config("C3A", 100_000, 130.0, 5, 1920, 1080, 70.0, 10),
+    "C3T": Config("C3T", 100_000, 130.0, 5, 1920, 1080, 70.0, 10),
 }
 
 
@@ -469,6 +494,14 @@ def trajectory(cfg: Config, n_frames: int | None = None):
         a = look_at_rig(c + np.array([0.35 * s, 0.0, 1.7]), c, 0.064)
         b = look_at_rig(c + np.array([0.35 * s, 0.0, 60.0]), c, 0.064)
         return [a if f < n // 2 else b for f in range(n)]
+    if cfg.name in ("C3A", "C3T"):
+        n = n_frames or 300
+        if cfg.name == "C3A":
+            steps = [0.2 + (40.0 - 0.2) * f / max(1, n - 1) for f in range(n)]
+        else:
+            steps = [1.0 if f < n // 3 else (10.0 if f < 2 * n // 3 else 35.0) for f in range(n)]
+        return make_pan(c + np.array([0.25 * s, 0.05 * s, 1.7]), c + np.array([0.05 * s, 0.05 * s, 1.7]),
+                        180.0, steps)
     if name == "C3":
         return make_orbit(c, 0.35 * s, 0.35 * s, 1.7, 60.0, n_frames or 300, 0.3)
     if name == "C4":

@@ -66,8 +66,9 @@ def compare_splats_pairs(o, r):
         og, orec = og[keep], orec[keep]
         m = (eye == e) & (sp[:, 12] > 0)          # splats with >= 1 kept tile
         assert np.array_equal(sg[m], og), f"splat set of eye {e} differs ({m.sum()} vs {len(og)})"
-        # u v A B C alpha r g b depth thr, and the kept-tile count
-        assert np.array_equal(sp[m][:, :11], orec[:, :11]), f"splat records of eye {e} differ"
+        # u v A B C alpha r g b depth, and the kept-tile count (the extent thr is not kept per splat on the
+        # GPU; it decides the kept tiles, which are compared here and in the sorted keys)
+        assert np.array_equal(sp[m][:, :10], orec[:, :10]), f"splat records of eye {e} differ"
         assert np.array_equal(sp[m][:, 12], orec[:, 11]), f"kept-tile counts of eye {e} differ"
     ok, og = o.pairs()
     gk, gg = r.debug("pairs"), r.debug("pair_g")

@@ -303,3 +303,34 @@ def test_build_cov_closed_forms(orc):
 
 
 orc_build_cov_declared = True
+
+
+def test_f3_trajectories_separate_the_guides(orc):
+    """F3 study inputs ("movement with acceleration and with staged speed changes"): on the staged
+    head-turn trajectory C3T the novelty rate rises stage by stage (~1% -> ~9% -> ~30%), and the three
+    guiding functions then choose different depths: all keep D_max in the slow stage, and in the fast
+    stage (novelty ~30%) H_staged = ceil(D/4) = 3 < H_exp = D >> 1 = 5 < H_linear = 1 + round(9 x 0.7) = 7
+    (R23 / Eq. 4), with the update rate ordered the other way."""
+    cfg = sg.config("C3T")
+    sc = cfg.scene()
+    traj = sg.trajectory(cfg)
+    res = {}
+    for guide in (0, 1, 2):
+        o = orc.Oracle(sc, orc.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, 10, guide=guide))
+        nov, dep, upd = [], [], []
+        for rig in traj:
+            st = o.frame(rig, raster=False).stats
+            nov.append(st.n_new / max(1, st.n_visible))
+            dep.append(st.depth_next)
+            upd.append(st.n_misses / max(1, st.n_visible))
+        res[guide] = [np.array(x) for x in (nov, dep, upd)]
+    nov = res[0][0]
+    n3 = len(nov) // 3
+    stage = [nov[1:n3].mean(), nov[n3 + 5:2 * n3].mean(), nov[2 * n3 + 5:].mean()]
+    assert stage[0] < 0.03 < stage[1] < 0.15 < stage[2]
+    for g in (0, 1, 2):
+        assert np.all(res[g][1][1:n3] == 10)                 # slow stage: every guide keeps D_max
+    mean_fast = {g: res[g][1][2 * n3 + 5:].mean() for g in (0, 1, 2)}
+    upd_fast = {g: res[g][2][2 * n3 + 5:].mean() for g in (0, 1, 2)}
+    assert mean_fast[2] < mean_fast[1] < mean_fast[0]
+    assert upd_fast[2] > upd_fast[1] > upd_fast[0]

@@ -7,7 +7,7 @@ S:260) by MSE / PSNR / SSIM, plus average and 99% FPS of each
 Variants: method (linear H, D_max from the config), no reuse (D_max = 1, the reference itself),
 exponential / staged guiding functions (R23), fixed 3-sigma extent and AABB tiles.
 
-  PYTHONPATH=. python tools/quality.py [config] [frames] [out.json]
+  PYTHONPATH=. python tools/quality.py [config] [frames] [out.json] [variant,variant,...]
 
 The metrics are measurement code (torch ops on the rendered images), not part of the hot path.
 """
@@ -54,7 +54,7 @@ def ssim(a, b) -> float:
     return float(s.mean())
 
 
-def run(config="C3", frames=150):
+def run(config="C3", frames=150, only=None):
     import torch
     import scenegen as sg
     import paper_2502_14938_b200 as gp
@@ -71,6 +71,8 @@ def run(config="C3", frames=150):
         "no_reuse": (1, 0),
         "no_dered": (cfg.d_max, "per_eye"),      # one monocular pipeline per eye (F1)
     }
+    if only:
+        variants = {k: v for k, v in variants.items() if k in only}
     # reference images: uncached (D_max = 1), opacity-aware extent, exact tiles
     ref_r = gp.Renderer(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, 1).load(sc)
     refs = []
@@ -88,7 +90,7 @@ def run(config="C3", frames=150):
         R = gp.PerEyeRenderer if per_eye else gp.Renderer
         r = R(0, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, dmax,
               flags=flags | gp.GSC_F_STAGE_TIMING | gp.GSC_F_SERIAL, pair_capacity=cap).load(sc)
-        ps, ss, ms_, misses, pairs = [], [], [], [], []
+        ps, ss, ms_, misses, pairs, depth, novelty = [], [], [], [], [], [], []
         for (rig, (rl, rr)) in zip(traj, refs):
             gl, gr, st = r.render(rig)
             p = min(psnr(gl, rl), psnr(gr, rr))
@@ -97,6 +99,8 @@ def run(config="C3", frames=150):
             sts = st if isinstance(st, list) else [st]
             misses.append(sum(x["n_misses"] for x in sts) / max(1, sum(x["n_visible"] for x in sts)))
             pairs.append(sum(x["n_pairs"] for x in sts))
+            depth.append(sts[0]["depth_next"])
+            novelty.append(sts[0]["novelty_rate"])
             ms_.append(sum(x["ms_total"] for x in sts))
         ms_ = np.array(ms_)
         out["variants"][name] = {
@@ -106,8 +110,12 @@ def run(config="C3", frames=150):
             "update_rate_mean": round(float(np.mean(misses)), 4), "pairs_mean": round(float(np.mean(pairs))),
             "fps_avg": round(float(1000.0 / np.mean(ms_)), 2) if len(ms_) else None,
             "fps_99pct": round(float(1000.0 / np.percentile(ms_, 99)), 2) if len(ms_) else None,
+            # per-frame traces (cache depth and update rate along the trajectory)
+            "trace": {"depth_next": [int(d) for d in depth], "update_rate": [round(float(m), 4) for m in misses],
+                      "novelty_rate": [round(float(n), 4) for n in novelty],
+                      "psnr_db": [round(float(p), 2) for p in ps], "ms": [round(float(m), 4) for m in ms_]},
         }
-        print(name, json.dumps(out["variants"][name]), flush=True)
+        print(name, json.dumps({k: v for k, v in out["variants"][name].items() if k != "trace"}), flush=True)
         del r
         torch.cuda.empty_cache()
     return out
@@ -116,7 +124,8 @@ def run(config="C3", frames=150):
 def main():
     config = sys.argv[1] if len(sys.argv) > 1 else "C3"
     frames = int(sys.argv[2]) if len(sys.argv) > 2 else 150
-    res = run(config, frames)
+    only = sys.argv[4].split(",") if len(sys.argv) > 4 else None
+    res = run(config, frames, only)
     if len(sys.argv) > 3:
         with open(sys.argv[3], "w") as fh:
             json.dump(res, fh, indent=1)
