@@ -4,9 +4,12 @@ rendering workers (each owning a private GS-Cache pipeline: its own `Renderer`, 
 FPS-band controller that starts a worker below Min-FPS and stops one above (1 + 1/N) Max-FPS, and
 display-order synchronisation that drops frames older than the last one written.
 
-Two clock modes: ``run_session(..., clock="sim")`` drives the identical control logic
+Three modes: ``run_session(..., clock="sim")`` drives the identical control logic
 single-threaded on a virtual clock with injected per-frame costs (deterministic, for tests);
-``clock="real"`` runs one thread per worker on the wall clock, each rendering through the C ABI.
+``clock="proc"`` is the paper's deployment ("the scheduler starts a new rendering worker
+process"): one OS process per worker, each owning a private pipeline (its own CUDA context, scene copy
+and cache on GPU w mod n_gpus), fed by the coordinator's shared queue; ``clock="real"`` runs the
+workers as threads of one process (same logic, cheaper start-up).
 
 Readings (R25): FPS = last 30 displayed frames / their time span; control period 0.5 s with
 at most one action; pose thresholds 0.01 m / 0.5 degree; queue capacity 8, timeout 100 ms; the
@@ -206,11 +209,17 @@ def _report(records, displayed_t, timeline, queue):
 
 def run_session(trajectory, cfg: SessionConfig, clock: str = "sim",
                 cost_fn: Optional[Callable[[int, int, float], float]] = None,
-                make_worker: Optional[Callable[[int], Callable]] = None, duration: Optional[float] = None):
+                make_worker: Optional[Callable[[int], Callable]] = None, duration: Optional[float] = None,
+                worker_spec: Optional[tuple] = None, prewarm: bool = True):
     """Alg. 2 top-level loop.  trajectory: list of rigs sampled every cfg.sample_interval.
     clock="sim": virtual time; worker w renders a frame submitted at t in cost_fn(w, frame, t) seconds.
     clock="real": wall time; make_worker(w) returns render(rig) -> stats dict (one private pipeline
-    per worker, e.g. a Renderer on its own GPU)."""
+    per worker, e.g. a Renderer on its own GPU).
+    clock="proc": wall time, one process per worker; worker_spec = (module, function, kwargs) names a
+    module-level factory function(w, **kwargs) -> render(rig), called inside the worker process.  With
+    prewarm (default) all w_max worker processes build their pipelines (scene load: seconds at city
+    scale) before the clock starts and the controller activates / deactivates them, so a start takes
+    effect at once; without it a start spawns the process and the worker joins when its scene is loaded."""
     queue = CameraQueue(cfg.timeout, cfg.capacity, cfg.delta_p, cfg.delta_theta_deg)
     ctrl = FpsController(cfg.min_fps, cfg.max_fps, cfg.w_max, cfg.window, cfg.control_period)
     ctrl.n_workers = cfg.w_init
@@ -222,6 +231,8 @@ def run_session(trajectory, cfg: SessionConfig, clock: str = "sim",
         return _run_sim(trajectory, cfg, queue, ctrl, sync, meter, cost_fn, duration)
     if clock == "real":
         return _run_real(trajectory, cfg, queue, ctrl, sync, meter, make_worker, duration)
+    if clock == "proc":
+        return _run_proc(trajectory, cfg, queue, ctrl, sync, meter, worker_spec, duration, prewarm)
     raise ValueError(clock)
 
 
@@ -364,3 +375,182 @@ def _run_real(trajectory, cfg, queue, ctrl, sync, meter, make_worker, duration):
     if errors:
         raise RuntimeError("rendering worker failed; session aborted") from errors[0]
     return _report(records, displayed, timeline, queue)
+
+
+# ------------------------------------------------------------------ process workers
+def _worker_main(w, spec, tasks, results):
+    """Body of one rendering worker process: build the private pipeline, report ready, then render the
+    poses the coordinator hands over until told to stop (None)."""
+    import importlib
+    import os
+    try:
+        mod, fn, kw = spec
+        render = getattr(importlib.import_module(mod), fn)(w, **kw)
+        results.put(("ready", w, os.getpid(), None))
+        while True:
+            item = tasks.get()
+            if item is None:
+                break
+            k, rig = item
+            t0 = time.perf_counter()
+            st = render(rig)
+            results.put(("done", w, k, (t0, time.perf_counter(), st or {})))
+    except BaseException as exc:   # reported to the coordinator, which aborts the session (S:466)
+        results.put(("error", w, None, repr(exc)))
+    results.put(("exit", w, None, None))
+
+
+def _run_proc(trajectory, cfg, queue, ctrl, sync, meter, spec, duration, prewarm=True):
+    """The coordinator: samples poses into the shared queue, hands the head of the queue to each idle
+    worker process (Alg. 2: a worker takes the next camera when it finishes the previous one), displays in
+    timestamp order, and runs the FPS-band controller, starting / stopping worker processes.  Times are
+    CLOCK_MONOTONIC (time.perf_counter), shared by all processes of the machine."""
+    import multiprocessing as mp
+    assert spec is not None
+    ctx = mp.get_context("spawn")
+    results = ctx.Queue()
+    procs, tasks = {}, {}
+    ready, idle, busy = set(), [], {}
+    pids = {}
+    records, displayed = [], []
+    order = []
+
+    def start(w):
+        tasks[w] = ctx.Queue()
+        p = ctx.Process(target=_worker_main, args=(w, spec, tasks[w], results), daemon=True)
+        p.start()
+        procs[w] = p
+        order.append(w)
+
+    n_spawn = cfg.w_max if prewarm else ctrl.n_workers
+    for w in range(n_spawn):
+        start(w)
+    standby = []                       # prewarmed workers not yet activated (ascending id)
+    del order[ctrl.n_workers:]
+    # the spawned workers' pipelines are built before the clock starts (setup, not session time)
+    while len(ready) < n_spawn:
+        kind, w, a, b = results.get(timeout=900)
+        if kind == "error":
+            raise RuntimeError(f"worker {w} failed to start: {b}")
+        if kind == "ready":
+            ready.add(w)
+            pids[w] = a
+    idle.extend(range(ctrl.n_workers))
+    standby.extend(range(ctrl.n_workers, n_spawn))
+    t0 = time.perf_counter()
+    now = lambda: time.perf_counter() - t0  # noqa: E731
+    timeline = [(0.0, len(order))]
+    stopping = set()
+    k = 0
+    next_ctrl = cfg.control_period
+    jobs = {}
+    err = None
+    while err is None:
+        t = now()
+        if t >= duration:
+            break
+        while k < len(trajectory) and k * cfg.sample_interval <= t:
+            queue.submit_pose(trajectory[k], t)
+            k += 1
+        # hand work to idle workers (head of the queue, stale entries dropped)
+        while idle:
+            e = queue.take_work(now())
+            if e is None:
+                break
+            w = idle.pop(0)
+            jobs[w] = (e, now())
+            tasks[w].put((len(records) + len(jobs), e.rig))
+        try:
+            kind, w, a, b = results.get(timeout=0.0005)
+        except Exception:
+            kind = None
+        if kind == "done":
+            e, ts = jobs.pop(w)
+            te = now()
+            shown = sync.try_display(e.timestamp)
+            records.append(FrameRecord(e.timestamp, w, ts, te, shown, dict(b[2], pid=pids.get(w))))
+            if shown:
+                meter.add(te)
+                displayed.append(te)
+            if w in stopping:
+                stopping.discard(w)
+                if prewarm:
+                    standby.insert(0, w)
+                else:
+                    tasks[w].put(None)
+            else:
+                idle.append(w)
+        elif kind == "ready":
+            ready.add(w)
+            pids[w] = a
+            if w in order:
+                idle.append(w)
+        elif kind == "error":
+            err = RuntimeError(f"rendering worker {w} failed: {b}")
+        if cfg.control and t >= next_ctrl:
+            act = ctrl.control_step(meter.fps(), t)
+            if act == START:
+                if standby:
+                    w = standby.pop(0)
+                    order.append(w)
+                    idle.append(w)
+                else:
+                    start(len(procs))
+            elif act == STOP:
+                w = order.pop()                # LIFO; a busy worker finishes its frame first
+                if w in idle:
+                    idle.remove(w)
+                    if prewarm:
+                        standby.insert(0, w)
+                    else:
+                        tasks[w].put(None)
+                else:
+                    stopping.add(w)
+            if act is not NONE:
+                timeline.append((t, len(order)))
+            next_ctrl += cfg.control_period
+    for w, p in procs.items():
+        if p.is_alive():
+            tasks[w].put(None)
+    for p in procs.values():
+        p.join(timeout=60)
+        if p.is_alive():
+            p.terminate()
+    if err is not None:
+        raise err
+    rep = _report(records, displayed, timeline, queue)
+    rep.worker_pids = dict(pids)
+    return rep
+
+
+def sleep_worker(w, cost: float = 0.01, cost_by_worker: Optional[dict] = None):
+    """A synthetic rendering worker for CPU tests and simulations of the process mode: "renders" a pose
+    by sleeping `cost` seconds (or cost_by_worker[w])."""
+    c = (cost_by_worker or {}).get(w, cost)
+
+    def render(rig):
+        time.sleep(c)
+        return {"cost": c}
+    return render
+
+
+def gsc_worker(w, config: str = "C4", fmt_rgba8: bool = True):
+    """A GS-Cache rendering worker: its own Renderer (scene copy, cache, streams) on GPU w mod n_gpus,
+    rendering each pose end to end into its pinned host images."""
+    import torch
+    import scenegen as sg
+    import paper_2502_14938_b200 as gp
+    cfg = sg.config(config)
+    dev = w % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    r = gp.Renderer(dev, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max).load(cfg.scene())
+    fmt = gp.GSC_FMT_RGBA8 if fmt_rgba8 else gp.GSC_FMT_RGB_F32_PLANAR
+    shape = (cfg.height, cfg.width, 4) if fmt_rgba8 else (3, cfg.height, cfg.width)
+    dt = torch.uint8 if fmt_rgba8 else torch.float32
+    hl = torch.empty(shape, dtype=dt).pin_memory()
+    hr = torch.empty(shape, dtype=dt).pin_memory()
+
+    def render(rig):
+        r.render_host(rig, hl, hr, fmt)
+        return {"device": dev}
+    return render

@@ -461,6 +461,9 @@ CONFIGS = {
     # per frame, 100 frames each) -- the novelty rate then spans 0 -> ~30%, where the guides differ
     "C3A": Config("C3A", 100_000, 130.0, 5, 1920, 1080, 70.0, 10),
     "C3T": Config("C3T", 100_000, 130.0, 5, 1920, 1080, 70.0, 10),
+    # SURVEY §8(f) F2 zoom-out experiment: the C5 city, the camera pointing at the centre and
+    # moving away from it (40 m -> 1800 m along a rising diagonal, 600 frames)
+    "C5Z": Config("C5Z", 5_000_000, 900.0, 5, 1920, 1080, 70.0, 10),
 }
 
 
@@ -494,6 +497,12 @@ def trajectory(cfg: Config, n_frames: int | None = None):
         a = look_at_rig(c + np.array([0.35 * s, 0.0, 1.7]), c, 0.064)
         b = look_at_rig(c + np.array([0.35 * s, 0.0, 60.0]), c, 0.064)
         return [a if f < n // 2 else b for f in range(n)]
+    if cfg.name == "C5Z":
+        n = n_frames or 600
+        d = np.array([-1.0, -0.6, 0.7])
+        d /= np.linalg.norm(d)
+        return [look_at_rig(c + d * (40.0 + (1800.0 - 40.0) * f / max(1, n - 1)), c, 0.064, t=f / 90.0)
+                for f in range(n)]
     if cfg.name in ("C3A", "C3T"):
         n = n_frames or 300
         if cfg.name == "C3A":

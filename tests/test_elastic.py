@@ -114,3 +114,27 @@ def test_hysteresis_no_change_inside_band():
     cfg = el.SessionConfig(min_fps=60, max_fps=120, w_max=3, sample_interval=0.005, timeout=1.0)
     rep = el.run_session(_traj(4000), cfg, clock="sim", cost_fn=lambda w, f, t: 0.010)   # ~100 FPS
     assert len(rep.worker_timeline) == 1
+
+
+@pytest.mark.slow
+def test_process_workers_elastic_start_and_stop():
+    """workers are OS processes.  With every worker taking 40 ms per frame (25 FPS per worker)
+    the controller starts worker processes up to w_max; frames come from several distinct processes,
+    displayed timestamps stay monotone, no displayed frame is older than the timeout when its render
+    started.  Then with 2 ms frames (~450 FPS at 1 worker pace > (1 + 1/N) Max) it stops them again."""
+    rigs = [_rig(0.02 * k) for k in range(2000)]
+    cfg = el.SessionConfig(min_fps=60, max_fps=120, w_max=3, w_init=1, sample_interval=1 / 200.0,
+                           control_period=0.25, timeout=0.1)
+    rep = el.run_session(rigs, cfg, clock="proc", duration=2.5,
+                         worker_spec=("paper_2502_14938_b200.elastic", "sleep_worker", {"cost": 0.040}))
+    assert max(n for _, n in rep.worker_timeline) == 3
+    pids = {r.stats["pid"] for r in rep.records}
+    assert len(pids) == 3 and all(p != __import__("os").getpid() for p in pids)
+    ts = rep.displayed_ts
+    assert len(ts) > 40 and all(a <= b for a, b in zip(ts, ts[1:]))
+    assert all(r.t_start - r.timestamp <= cfg.timeout + 0.02 for r in rep.records)
+    cfg2 = el.SessionConfig(min_fps=60, max_fps=120, w_max=3, w_init=3, sample_interval=1 / 500.0,
+                            control_period=0.25, timeout=0.1)
+    rep2 = el.run_session(rigs, cfg2, clock="proc", duration=2.0,
+                          worker_spec=("paper_2502_14938_b200.elastic", "sleep_worker", {"cost": 0.002}))
+    assert min(n for _, n in rep2.worker_timeline) == 1
