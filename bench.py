@@ -98,8 +98,9 @@ def _stage_bytes(s, N, K, W, H, fmt_bytes):
     """Algorithmic HBM bytes per stage for one frame."""
     V, M, C, P = s["n_visible"], s["n_misses"], s["n_splats"], s["n_pairs"]
     return {
-        # pos_m 16 + level 1 + birth 4 per anchor, bitsets, ids out, birth writes
-        "cull": N * (16 + 1 + 4) + N / 4.0 + 4 * V + 8 * M,
+        # pos_m 16 + level 1 per anchor, bitsets; the cache line (birth, 4 B) of each visible anchor; ids
+        # out, birth writes of the misses
+        "cull": N * (16 + 1) + N / 4.0 + 4 * V + 4 * V + 8 * M,
         # miss id, pos, feat, offs, scale in; alpha + 48-byte pool record out per slot
         "derive": M * (4 + 16 + 32 + 120 + 12) + M * K * (4 + 48),
         # SURVEY d-3: visible ids + 4 B alpha per visible slot, 48-byte pool record per live Gaussian read;

@@ -15,8 +15,8 @@
 //
 // Layout: pos_m float4[N] = (x, y, z, m_i) -- one 16-byte coalesced load per
 // anchor; level u8[N]; birth i32[N]; bitsets u32[ceil(N/32)] (visibility: ping-pong; misses).
-// HBM bytes per anchor: 16 + 1 + 4 + 1/8 (+4 per miss birth write, +4 per
-// visible id, +4 per miss id).
+// HBM bytes per anchor: 16 + 1 + 1/8 (+4 birth read per visible anchor -- the cache line is looked up
+// only for visible anchors --, +4 per miss birth write, +4 per visible id, +4 per miss id).
 #include "gsc_internal.cuh"
 
 namespace gsc {
@@ -69,25 +69,34 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
   const int32_t f = pol->frame, W = pol->W;
   const int64_t wbase = (int64_t)tile * kCullTile + warp * (32 * kCullItems);
 
-  // all of the thread's anchor loads in flight before the first predicate
+  // all of the thread's anchor loads in flight before the first predicate (and the previous frame's
+  // visibility words of the warp's 8 groups: lane k holds group k's)
   float4 pm[kCullItems];
   int lv[kCullItems];
-  int32_t bi[kCullItems];
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
     const int64_t i = wbase + it * 32 + lane;
     pm[it] = i < N ? pos_m[i] : make_float4(0.f, 0.f, 0.f, 0.f);
     lv[it] = i < N ? level[i] : 0;
-    bi[it] = i < N ? birth[i] : 0;
+  }
+  const uint32_t pw_lane =
+      (lane < (uint32_t)kCullItems && wbase + lane * 32 < N) ? prev_vis[(wbase >> 5) + lane] : 0u;
+  // predicates first; the cache lines (birth) are read for the visible anchors only, all in flight
+  bool vis[kCullItems];
+  int32_t bi[kCullItems];
+#pragma unroll
+  for (int it = 0; it < kCullItems; ++it) {
+    const int64_t i = wbase + it * 32 + lane;
+    vis[it] = i < N && cull_visible(u, pm[it], lv[it], L, d0);
+    bi[it] = vis[it] ? birth[i] : 0;
   }
   uint32_t cnt_v = 0, cnt_m = 0, cnt_new = 0;
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
     const int64_t i = wbase + it * 32 + lane;
-    bool vis = false, miss = false;
-    if (i < N) {
-      vis = cull_visible(u, pm[it], lv[it], L, d0);
-      if (vis) {
+    bool miss = false;
+    if (vis[it]) {
+      {
         miss = !(bi[it] > W);
         // derived this frame (Alg. 1 "update computation cache"); GSC_F_STAGGER (R26): a line filled
         // for the first time since the reset (birth INT32_MIN) is back-dated by min(i mod D, f-1-W)
@@ -101,11 +110,11 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
         }
       }
     }
-    const uint32_t mv = __ballot_sync(0xFFFFFFFFu, vis);
+    const uint32_t mv = __ballot_sync(0xFFFFFFFFu, vis[it]);
     const uint32_t mm = __ballot_sync(0xFFFFFFFFu, miss);
     const int64_t word = (wbase + it * 32) >> 5;
+    const uint32_t pw = __shfl_sync(0xFFFFFFFFu, pw_lane, it);
     if (wbase + it * 32 < N) {
-      const uint32_t pw = prev_vis[word];
       if (lane == 0) { cur_vis[word] = mv; miss_bits[word] = mm; }
       cnt_new += __popc(mv & ~pw);
     }
