@@ -447,12 +447,13 @@ __global__ void __launch_bounds__(kMThreads, 1) derive_mma_kernel(DeriveArgs p) 
     phase ^= 1;
     tc_fence_after();
 
-    // ---- epilogue 1 (warps 0-3: TMEM lane quarter = warp): bias, ReLU, byte limbs -> layer-2 A tiles
-    if (warp < 4) {
-      const int row = warp * 32 + lane;
-      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    // ---- epilogue 1 (all 16 warps: warp w reads TMEM lane quarter w % 4 -- the quarter tcgen05.ld allows
+    // it -- and the 16-column chunks c = w / 4, w / 4 + 4): bias, ReLU, byte limbs -> layer-2 A tiles
+    {
+      const int q = warp & 3, row = q * 32 + lane;
+      const uint32_t lane_base = (uint32_t)(q * 32) << 16;
 #pragma unroll 1
-      for (int c = 0; c < 6; ++c) {          // 16 hidden units per chunk
+      for (int c = warp >> 2; c < 6; c += 4) {   // 16 hidden units per chunk
         uint32_t r[16];
         tmem_ld16(tmem + lane_base + kD1Col + 16 * c, r);
         tmem_wait_ld();
@@ -493,16 +494,19 @@ __global__ void __launch_bounds__(kMThreads, 1) derive_mma_kernel(DeriveArgs p) 
     phase ^= 1;
     tc_fence_after();
 
-    // ---- epilogue 2 (warps 0-3): z2 = sum_l 256^l D2[h][l] + 2^14 b2; o = fp32(z2) 2^-21 -> SMEM
-    if (warp < 4) {
-      const int row = warp * 32 + lane;
-      const uint32_t lane_base = (uint32_t)(warp * 32) << 16;
+    // ---- epilogue 2 (all 16 warps, lane quarter w % 4, the 8 column chunks of the three heads -- 1 | 2 | 5
+    // of 16 -- dealt round-robin to the quarter's 4 warps): z2 = sum_l 256^l D2[h][l] + 2^14 b2;
+    // o = fp32(z2) 2^-21 -> SMEM
+    {
+      const int q = warp & 3, row = q * 32 + lane;
+      const uint32_t lane_base = (uint32_t)(q * 32) << 16;
 #pragma unroll 1
-      for (int h = 0; h < 3; ++h) {
+      for (int ck = warp >> 2; ck < 8; ck += 4) {
+        const int h = ck == 0 ? 0 : (ck < 3 ? 1 : 2);
+        const int c = 16 * (ck == 0 ? 0 : (ck < 3 ? ck - 1 : ck - 3));
         const int nh = h == 0 ? kK : (h == 1 ? 3 * kK : 7 * kK);
         const int mo = h == 0 ? 0 : (h == 1 ? kK : 4 * kK);
-#pragma unroll 1
-        for (int c = 0; c < d2_npad(h); c += 16) {
+        {
           uint32_t r0[16], r1[16], r2[16];
           tmem_ld16(tmem + lane_base + d2_col(h, 0) + c, r0);
           tmem_ld16(tmem + lane_base + d2_col(h, 1) + c, r1);
