@@ -137,14 +137,28 @@ def run_gsc(args):
     fmt = gp.GSC_FMT_RGBA8
     free0 = torch.cuda.mem_get_info(dev)[0]
     base = (gp.GSC_F_STAGGER if args.stagger else 0) | (gp.GSC_F_BLEND_EXACT if args.blend_exact else 0)
+    eye_split = args.mode == "eye-split"
+    if eye_split:                                   # SURVEY §8(e) latency mode: one eye per rank (GSC_F_MONO)
+        base |= gp.GSC_F_MONO
     r = gp.Renderer(local, cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max,
                     flags=base, pair_capacity=args.pair_capacity).load(sc)
     torch.cuda.synchronize()
     mem_bytes = free0 - torch.cuda.mem_get_info(dev)[0]   # the context's device memory (scene, cache, frames)
     out_l, out_r = r.alloc_outputs(fmt)
     stream = torch.cuda.current_stream(dev)
-    frames = multi.frame_block(rank, world, len(traj), args.steps)
-    warm = multi.frame_block(rank, world, len(traj), args.warmup)
+    if eye_split:
+        eye, frames = multi.eye_split(rank, world, len(traj), args.steps)
+        warm = multi.eye_split(rank, world, len(traj), args.warmup)[1]
+        traj = [gp.PerEyeRenderer._mono(rig, eye) for rig in traj]
+    else:
+        frames = multi.frame_block(rank, world, len(traj), args.steps)
+        warm = multi.frame_block(rank, world, len(traj), args.warmup)
+    # optional final image gather to rank 0 every frame: the one collective
+    gather = args.gather and world > 1
+
+    def gather_frame():
+        if gather:
+            multi.gather_images(out_l if not share else out_l.cpu())
 
     # warm-up, then a cold cache for the timed block (frame 0 of the block decodes everything)
     for f in warm:
@@ -161,6 +175,7 @@ def run_gsc(args):
     e0.record(stream)
     for f in frames:
         r.render_into(traj[f], out_l, out_r, fmt, stream)
+        gather_frame()
     e1.record(stream)
     torch.cuda.synchronize()
     multi.barrier()
@@ -210,7 +225,7 @@ def run_gsc(args):
     counted = replay(gp.GSC_F_COUNT_EVALS)
     r.set_flags(base)
 
-    total_frames = world * len(frames)
+    total_frames = (world // 2 if eye_split else world) * len(frames)
     value = total_frames / (t_max / 1000.0) if t_max > 0 else 0.0
 
     # per-stage measured ms (CUDA events inside the timed region) and roofline
@@ -286,7 +301,9 @@ def run_gsc(args):
                        "anchors": sc.n, "width": cfg.width, "height": cfg.height, "d_max": cfg.d_max,
                        "frames_per_rank": len(frames), "out_format": "rgba8",
                        "l2": "no flush: per-frame working set (pool/splat/pair traffic ~1-2 GB) > 126 MB L2",
-                       "parallelism": f"frames partitioned by view, scene replicated, dp{world}",
+                       "parallelism": (f"eye split: {world // 2} rank pairs, left / right eye per rank"
+                                       if eye_split else f"frames partitioned by view, scene replicated, dp{world}")
+                                      + (", RGBA8 image gathered to rank 0 every frame" if gather else ""),
                        **({"variant": "staggered expiry (GSC_F_STAGGER, F3)"} if args.stagger else {}),
                        **({"blend": "exact exponential (GSC_F_BLEND_EXACT)"} if args.blend_exact else {})},
             "stages": stage_report,
@@ -389,6 +406,9 @@ def main():
     ap.add_argument("--pair-capacity", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--stagger", action="store_true", help="staggered expiry variant (GSC_F_STAGGER, SURVEY 8(f) F3)")
+    ap.add_argument("--mode", default="throughput", choices=["throughput", "eye-split"],
+                    help="multi-GPU partition: frame blocks per rank, or one eye per rank (latency mode)")
+    ap.add_argument("--gather", action="store_true", help="gather each frame's image to rank 0 (NCCL)")
     ap.add_argument("--blend-exact", action="store_true", help="blend with exp_s on every evaluation (GSC_F_BLEND_EXACT)")
     ap.add_argument("--cpu-sample-frames", type=int, default=1)
     ap.add_argument("--ref-frames", type=int, default=4)
