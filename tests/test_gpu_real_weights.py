@@ -98,3 +98,33 @@ def test_gsc2_v3_file(orc, tmp_path):
         hl, _, _ = rh.render(rig)
         assert np.array_equal(rf.debug("pool"), rh.debug("pool"))
         assert np.array_equal(fl.cpu().numpy(), hl.cpu().numpy())
+
+
+def test_real_weights_load_errors(tmp_path):
+    """gsc_load_scene_host_f32 / GSC2 v3: a non-finite feature or weight -> GSC_EFORMAT; a level >= L ->
+    GSC_EFORMAT; a truncated v3 file -> GSC_EFORMAT with the offset of the array that does not fit."""
+    import copy
+    import re
+    from paper_2502_14938_b200 import _abi
+    cfg = sg.config("C1R")
+    sc = cfg.scene()
+    for name in ("feat", "W1", "b2s"):
+        bad = copy.copy(sc)
+        arr = getattr(sc, name).copy()
+        arr.flat[3] = np.nan
+        setattr(bad, name, arr)
+        with pytest.raises(_abi.GscError) as ei:
+            renderer(cfg).load(bad)
+        assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
+    path = str(tmp_path / "r.gsc2")
+    sg.write_gsc2(sc, path)
+    data = open(path, "rb").read()
+    n = sc.n
+    off_W1 = 56 + 12 * n + 128 * n + 120 * n + 12 * n + n      # pos, feat (f32), offs, scale, level
+    cut = str(tmp_path / "cut.gsc2")
+    with open(cut, "wb") as fh:
+        fh.write(data[:off_W1 + 100])
+    with pytest.raises(_abi.GscError) as ei:
+        renderer(cfg).load(cut)
+    assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
+    assert int(re.search(r"offset (\d+)", str(ei.value)).group(1)) == off_W1
