@@ -156,6 +156,33 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   for (uint32_t ch = gw; ch < nchunks; ch += nw) {
     const uint32_t q0 = ch * kExpChunk, q1 = min(q0 + kExpChunk, P) - 1;
     const uint32_t pa = warp_find(in.pair_off, C, q0), pb = warp_find(in.pair_off, C, q1);
+    if (pb - pa < 32) {   // warp-uniform: the chunk's splats fit one per lane (big splats, near the ground)
+      // the bracket's offsets, splat ids and list offsets in registers (coalesced loads), each position's
+      // splat by a 5-step shuffle search: one dependent global load per position instead of four
+      const uint32_t p = pa + lane;
+      const bool v = p <= pb;
+      const uint32_t off = v ? in.pair_off[p] : 0xFFFFFFFFu;
+      const uint32_t c = v ? in.sorted[p] : 0u;
+      const uint32_t lo = v ? in.list_off[c] : 0u;
+#pragma unroll
+      for (int i = 0; i < kExpItems; ++i) {
+        const uint32_t q = q0 + i * 32 + lane;
+        uint32_t l = 0;
+#pragma unroll
+        for (uint32_t st = 16; st; st >>= 1)
+          if (__shfl_sync(0xFFFFFFFFu, off, l + st) <= q) l += st;
+        const uint32_t oc = __shfl_sync(0xFFFFFFFFu, c, l), ol = __shfl_sync(0xFFFFFFFFu, lo, l),
+                       oo = __shfl_sync(0xFFFFFFFFu, off, l);
+        if (q <= q1) {
+          const uint32_t key = in.list[ol + (q - oo)];
+          keys_out[q] = key;
+          vals_out[q] = oc;
+          atomicAdd(&s_hist[0][key & tmask], 1u);          // the tile sort's two tbits-bit digits
+          atomicAdd(&s_hist[1][(key >> tbits) & tmask], 1u);
+        }
+      }
+      continue;
+    }
 #pragma unroll
     for (int i = 0; i < kExpItems; ++i) {
       const uint32_t q = q0 + i * 32 + lane;
