@@ -456,6 +456,7 @@ CONFIGS = {
     "C1R": Config("C1R", 1000, 20.0, 3, 64, 64, 70.0, 10, real=True),
     "C3R": Config("C3R", 100_000, 130.0, 5, 1920, 1080, 70.0, 10, real=True),
     "C3S": Config("C3S", 100_000, 130.0, 1, 1920, 1080, 70.0, 10, real=True),
+    "C4R": Config("C4R", 1_000_000, 400.0, 5, 1920, 1080, 70.0, 10, real=True),
     # SURVEY §8(f) F3 (depth-policy study): the C3 scene with a street-level head turn whose speed
     # accelerates (C3A: 0.2 -> 40 deg/frame over 300 frames) or changes in stages (C3T: 1 / 10 / 35 deg
     # per frame, 100 frames each) -- the novelty rate then spans 0 -> ~30%, where the guides differ

@@ -424,3 +424,32 @@ def test_blend_exact_mode_bit_identical(orc, c1):
     for rig in sg.trajectory(cfg):
         st, d = _frame_parity(orc, o, r, rig)
         assert d == 0.0
+
+
+def test_c4_full_size_blend_exact(orc, c4):
+    """GSC_F_BLEND_EXACT at configs[3] full size: frames 0 (cold) and 30 with pixels bit-identical to the
+    oracle (the default fast blend is checked against BLEND_FAST_TOL in test_c4_full_size_bench_config)."""
+    import paper_2502_14938_b200 as gp
+    cfg, sc = c4
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg, flags=gp.GSC_F_BLEND_EXACT).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(31):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in (0, 30))
+        if f in (0, 30):
+            assert d == 0.0
+
+
+def test_c5_high_altitude_block(orc):
+    """configs[4] near the end of its 2400-frame trajectory (~280 m, the widest views): a cold block from
+    frame 2300, full parity at 2300 and 2305, sets between."""
+    cfg = sg.config("C5")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(2300, 2306):
+        st, d = _frame_parity(orc, o, r, traj[f], full=f in (2300, 2305))
+        assert not st["overflow"]
+        if f in (2300, 2305):
+            assert d <= BLEND_FAST_TOL

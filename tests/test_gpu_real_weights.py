@@ -128,3 +128,18 @@ def test_real_weights_load_errors(tmp_path):
         renderer(cfg).load(cut)
     assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
     assert int(re.search(r"offset (\d+)", str(ei.value)).group(1)) == off_W1
+
+
+def test_c4r_real_weights_full_size(orc):
+    """The real-weights path at configs[3] size (1M anchors, 2K binocular): frame 0 (every visible anchor
+    derived by the fixed-order fp32 MLP: ~630k anchors) and frame 5 fully bit-exact up to the pixels.
+    (These weights give larger Gaussians than the grid scene's: frame 0 needs 40.2M pairs, above the
+    default capacity of 4 N K = 40M, so the context is created with a larger pair_capacity.)"""
+    cfg = sg.config("C4R")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg, pair_capacity=64 << 20).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(6):
+        st, _ = _frame(o, r, traj[f], full=f in (0, 5))
+        assert not st["overflow"]
