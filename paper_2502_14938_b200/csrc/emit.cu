@@ -9,10 +9,12 @@
 //   pairoff: exclusive scan of the kept-tile counts in depth order
 //            (CTA tiles of 4096, reduce-then-scan) -> pair_off[p], P
 //   expand : load-balanced expansion -- each warp owns 256 consecutive OUTPUT
-//            positions q and finds the owning splat by a 32-ary cooperative
-//            search of pair_off, so the heavy-tailed splat sizes (near splats
-//            are both the biggest and the first in depth order) cost nothing
-//            extra; reads of the list are contiguous runs, writes coalesced.
+//            positions q, brackets their splats [pa, pb] by a 32-ary cooperative
+//            search of pair_off (so the heavy-tailed splat sizes -- near splats
+//            are both the biggest and the first in depth order -- cost nothing
+//            extra), loads the bracket 32 splats at a time into registers and
+//            maps each position to its splat by a shuffle search; reads of the
+//            list are contiguous runs, writes coalesced.
 //            Fused: the 2 x 256-bin digit histogram of the tile keys.
 //   (ranges: derived by the last tile-digit pass of the sort, sort.cu)
 #include "gsc_internal.cuh"
@@ -156,24 +158,26 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
   for (uint32_t ch = gw; ch < nchunks; ch += nw) {
     const uint32_t q0 = ch * kExpChunk, q1 = min(q0 + kExpChunk, P) - 1;
     const uint32_t pa = warp_find(in.pair_off, C, q0), pb = warp_find(in.pair_off, C, q1);
-    if (pb - pa < 32) {   // warp-uniform: the chunk's splats fit one per lane (big splats, near the ground)
-      // the bracket's offsets, splat ids and list offsets in registers (coalesced loads), each position's
-      // splat by a 5-step shuffle search: one dependent global load per position instead of four
-      const uint32_t p = pa + lane;
+    // the chunk's splats [pa, pb] in groups of 32 (one per lane: offset, splat id and list offset in
+    // registers, coalesced loads); each position of the group's span finds its splat by a 5-step
+    // shuffle search: one dependent global load per position (the list key)
+    for (uint32_t g0 = pa; g0 <= pb; g0 += 32) {
+      const uint32_t p = g0 + lane;
       const bool v = p <= pb;
       const uint32_t off = v ? in.pair_off[p] : 0xFFFFFFFFu;
       const uint32_t c = v ? in.sorted[p] : 0u;
       const uint32_t lo = v ? in.list_off[c] : 0u;
-#pragma unroll
-      for (int i = 0; i < kExpItems; ++i) {
-        const uint32_t q = q0 + i * 32 + lane;
+      const uint32_t gs = max(q0, __shfl_sync(0xFFFFFFFFu, off, 0));
+      const uint32_t ge = g0 + 32 <= pb ? min(in.pair_off[g0 + 32], q1 + 1) : q1 + 1;   // exclusive
+      for (uint32_t qb = gs; qb < ge; qb += 32) {
+        const uint32_t q = qb + lane;
         uint32_t l = 0;
 #pragma unroll
         for (uint32_t st = 16; st; st >>= 1)
           if (__shfl_sync(0xFFFFFFFFu, off, l + st) <= q) l += st;
         const uint32_t oc = __shfl_sync(0xFFFFFFFFu, c, l), ol = __shfl_sync(0xFFFFFFFFu, lo, l),
                        oo = __shfl_sync(0xFFFFFFFFu, off, l);
-        if (q <= q1) {
+        if (q < ge) {
           const uint32_t key = in.list[ol + (q - oo)];
           keys_out[q] = key;
           vals_out[q] = oc;
@@ -181,23 +185,6 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
           atomicAdd(&s_hist[1][(key >> tbits) & tmask], 1u);
         }
       }
-      continue;
-    }
-#pragma unroll
-    for (int i = 0; i < kExpItems; ++i) {
-      const uint32_t q = q0 + i * 32 + lane;
-      if (q > q1) break;
-      uint32_t lo = pa, hi = pb;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (in.pair_off[mid] <= q) lo = mid; else hi = mid - 1;
-      }
-      const uint32_t c = in.sorted[lo];
-      const uint32_t key = in.list[in.list_off[c] + (q - in.pair_off[lo])];
-      keys_out[q] = key;
-      vals_out[q] = c;
-      atomicAdd(&s_hist[0][key & tmask], 1u);          // the tile sort's two tbits-bit digits
-      atomicAdd(&s_hist[1][(key >> tbits) & tmask], 1u);
     }
   }
   __syncthreads();
