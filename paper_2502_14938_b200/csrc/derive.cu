@@ -304,7 +304,7 @@ struct MmaSmem {
   alignas(128) uint8_t W1[96 * 64];          // layer-1 B: 96 x 64 B
   alignas(128) uint8_t A2[3][kMA * 96];      // layer-2 A limbs: 128 x 96 B (hidden, 3 heads)
   alignas(128) uint8_t W2[128 * 32];         // layer-2 B: head rows 16 | 32 | 80, 32 B each
-  float o[kMA][kNOut + 2];                   // layer-2 outputs
+  float o[kMA][kNOut + 1];                   // layer-2 outputs (odd row stride: the per-row writes of epilogue 2 hit 32 banks)
   int32_t b1s[96];
   int32_t b2s[kNOut];
   uint32_t anchor[kMA];

@@ -10,5 +10,5 @@ for k in range(16):
 torch.cuda.synchronize()
 print([h["n_misses"] for h in r.stats_history(16)])
 PY
-PYTHONPATH=. timeout 600 ncu --set full --clock-control none -k regex:derive_mma -o gpurun_out/$1/derive python /tmp/derive_frames.py > gpurun_out/$1/ncu_derive.txt 2>&1
+PYTHONPATH=. timeout 600 ncu --set full --clock-control none --import-source on -k regex:derive_mma ${NCU_EXTRA} -o gpurun_out/$1/derive python /tmp/derive_frames.py > gpurun_out/$1/ncu_derive.txt 2>&1
 tail -3 gpurun_out/$1/ncu_derive.txt
