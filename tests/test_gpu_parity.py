@@ -42,6 +42,21 @@ def test_c1_all_poses(orc, c1):
         assert d <= BLEND_FAST_TOL
 
 
+@pytest.mark.parametrize("wh", [(100, 70), (33, 17), (17, 129), (1, 1), (250, 4)])
+def test_c1_ragged_image_sizes(orc, c1, wh):
+    """Image sizes that are not multiples of the 16x16 tile nor of the 8x4 blend block (partial tiles and
+    blocks on the right and bottom edges, the row test's last-column special case, a 1x1 image, a 4-row
+    strip): every intermediate bit-exact, pixels within the blend tolerance, edge pixels included."""
+    import dataclasses
+    cfg, sc = c1
+    cfg = dataclasses.replace(cfg, width=wh[0], height=wh[1])
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    for rig in sg.trajectory(cfg):
+        st, d = _frame_parity(orc, o, r, rig)
+        assert d <= BLEND_FAST_TOL
+
+
 def test_c1_derive_on_cuda_cores(orc, c1):
     """The dp4a (CUDA-core) derivation path gives the same bits as the tcgen05 default."""
     from paper_2502_14938_b200 import _abi
