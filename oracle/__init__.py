@@ -30,6 +30,10 @@ Parity status per function:
                                 the exact rational on grid-valued inputs, within
                                 a derived bound of fp64 on real weights; epilogue
                                 shared with the grid path)
+  F4 combine inputs (R32)       pinned (one-hot logits reduce the bank to a
+                                single stride, exactly; fp64 softmax / blend /
+                                distance row within derived bounds; zero distance
+                                row == no distance input -- test_oracle_bank.py)
   depth-schedule shape H        parity unpinned beyond "linear"
 """
 from __future__ import annotations
@@ -69,7 +73,9 @@ class Scene(C.Structure):
                 ("W2c", C.c_void_p), ("b2c", C.c_void_p), ("W2s", C.c_void_p), ("b2s", C.c_void_p),
                 ("real", C.c_int), ("featf", C.c_void_p), ("W1f", C.c_void_p), ("b1f", C.c_void_p),
                 ("W2af", C.c_void_p), ("b2af", C.c_void_p), ("W2cf", C.c_void_p), ("b2cf", C.c_void_p),
-                ("W2sf", C.c_void_p), ("b2sf", C.c_void_p)]
+                ("W2sf", C.c_void_p), ("b2sf", C.c_void_p),
+                ("dist_input", C.c_int), ("bank", C.c_int), ("Wb1", C.c_void_p), ("bb1", C.c_void_p),
+                ("Wb2", C.c_void_p), ("bb2", C.c_void_p)]
 
 
 class Config(C.Structure):
@@ -133,6 +139,10 @@ def lib():
         L.orc_derive_anchor.argtypes = [C.POINTER(Scene), i32, vp, vp, vp, vp, vp, vp]
         L.orc_mlp_f32.argtypes = [C.POINTER(Scene), vp, vp]
         L.orc_mlp_f32.restype = None
+        L.orc_bank_weights.argtypes = [C.POINTER(Scene), vp, vp]
+        L.orc_bank_weights.restype = None
+        L.orc_bank_blend.argtypes = [vp, vp, vp]
+        L.orc_bank_blend.restype = None
         L.orc_derive_anchor.restype = None
         L.orc_project.argtypes = [C.POINTER(Config), C.POINTER(EyeConsts), f32, vp, vp, vp, C.POINTER(Splat)]
         L.orc_tile_kept.argtypes = [C.POINTER(Config), C.POINTER(Splat), i32, i32]
@@ -240,6 +250,14 @@ class SceneHolder:
             a = np.ascontiguousarray(getattr(sc, name), dtype=np.float32 if real else np.int8)
             self.arrays[name] = a
             setattr(s, name + "f" if real else name, a.ctypes.data)
+        # R32 combine inputs (real-weights scenes): distance input, feature bank
+        s.dist_input = int(real and bool(getattr(sc, "dist_input", False)))
+        s.bank = int(real and bool(getattr(sc, "bank", False)))
+        if s.bank:
+            for name in ("Wb1", "bb1", "Wb2", "bb2"):
+                a = np.ascontiguousarray(getattr(sc, name), dtype=np.float32)
+                self.arrays[name] = a
+                setattr(s, name, a.ctypes.data)
         self.s = s
 
 
@@ -255,11 +273,29 @@ def derive_anchor(sh: SceneHolder, i: int, pu):
 
 
 def mlp_f32(sh: SceneHolder, x) -> np.ndarray:
-    """The real-weights path's fixed-order fp32 MLP (F4): x[35] -> o[110]."""
+    """The real-weights path's fixed-order fp32 MLP (F4): x[35 + dist_input] -> o[110]."""
     x = np.ascontiguousarray(np.asarray(x, np.float32))
+    assert x.shape == (F + 3 + sh.s.dist_input,)
     o = np.zeros(NOUT, np.float32)
     lib().orc_mlp_f32(C.byref(sh.s), _p(x), _p(o))
     return o
+
+
+def bank_weights(sh: SceneHolder, y) -> np.ndarray:
+    """R32 feature-bank softmax weights (strides 4, 2, 1) for y = (d_view, distance)."""
+    y = np.ascontiguousarray(np.asarray(y, np.float32))
+    w = np.zeros(3, np.float32)
+    lib().orc_bank_weights(C.byref(sh.s), _p(y), _p(w))
+    return w
+
+
+def bank_blend(f, w) -> np.ndarray:
+    """R32 blended features fh[k] = fma(w2, f_k, fma(w1, f_{2 (k mod F/2)}, w0 f_{4 (k mod F/4)}))."""
+    f = np.ascontiguousarray(np.asarray(f, np.float32))
+    w = np.ascontiguousarray(np.asarray(w, np.float32))
+    fh = np.zeros(F, np.float32)
+    lib().orc_bank_blend(_p(f), _p(w), _p(fh))
+    return fh
 
 
 def project(cfg: Config, ec: EyeConsts, alpha, mu, cov, rgb):

@@ -308,11 +308,12 @@ void orc_build_cov(const float qin[4], const float S[3], float cov[6]) {
  * in ascending index order, one fused multiply-add (fmaf, one rounding) per term:
  *   h_c = max(0, fma(W1[34][c], x[34], ... fma(W1[0][c], x[0], b1[c])))
  *   o_m = fma(W2[31][m], h[31], ... fma(W2[0][m], h[0], b2[m]))   (h of the head of output m) */
-void orc_mlp_f32(const orc_scene *sc, const float x[F + 3], float o[ORC_NOUT]) {
+void orc_mlp_f32(const orc_scene *sc, const float *x, float o[ORC_NOUT]) {
   float a[3 * H];
+  const int nin = F + 3 + (sc->dist_input ? 1 : 0);
   for (int c = 0; c < 3 * H; ++c) {
     float acc = sc->b1f[c];
-    for (int k = 0; k < F + 3; ++k) acc = fmaf(sc->W1f[k * 3 * H + c], x[k], acc);
+    for (int k = 0; k < nin; ++k) acc = fmaf(sc->W1f[k * 3 * H + c], x[k], acc);
     a[c] = acc > 0.0f ? acc : 0.0f;            /* ReLU */
   }
   const float *W2[3] = {sc->W2af, sc->W2cf, sc->W2sf};
@@ -329,6 +330,39 @@ void orc_mlp_f32(const orc_scene *sc, const float x[F + 3], float o[ORC_NOUT]) {
   }
 }
 
+/* R32 feature bank (Scaffold-GS "first combine operator"; F4-B), written out in its
+ * fixed op order: hidden h_c = ReLU(bb1_c + sum_k Wb1[k][c] y_k) (one fma per term, k ascending from the
+ * bias); logits z_m = bb2_m + sum_c Wb2[c][m] h_c (same); softmax with the max subtracted:
+ * e_m = exp_s(z_m - max z), s = (e_0 + e_1) + e_2, w_m = e_m / s. */
+void orc_bank_weights(const orc_scene *sc, const float y[4], float w[3]) {
+  float h[F];
+  for (int c = 0; c < F; ++c) {
+    float acc = sc->bb1[c];
+    for (int k = 0; k < 4; ++k) acc = fmaf(sc->Wb1[k * F + c], y[k], acc);
+    h[c] = acc > 0.0f ? acc : 0.0f;
+  }
+  float z[3];
+  for (int m = 0; m < 3; ++m) {
+    float acc = sc->bb2[m];
+    for (int c = 0; c < F; ++c) acc = fmaf(sc->Wb2[c * 3 + m], h[c], acc);
+    z[m] = acc;
+  }
+  const float zmax = fmaxf(fmaxf(z[0], z[1]), z[2]);
+  float e[3];
+  for (int m = 0; m < 3; ++m) e[m] = orc_exp_s(z[m] - zmax);
+  const float s = (e[0] + e[1]) + e[2];
+  for (int m = 0; m < 3; ++m) w[m] = e[m] / s;
+}
+
+/* The three resolutions of the anchor feature: stride 1 (f itself), stride 2 and stride 4 -- every
+ * 2nd / 4th value, tiled back to F values -- blended as fma(w2, f_k, fma(w1, f2_k, w0 * f4_k)). */
+void orc_bank_blend(const float f[F], const float w[3], float fh[F]) {
+  for (int k = 0; k < F; ++k) {
+    const float f4 = f[4 * (k % (F / 4))], f2 = f[2 * (k % (F / 2))];
+    fh[k] = fmaf(w[2], f[k], fmaf(w[1], f2, w[0] * f4));
+  }
+}
+
 void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alpha, float *mu,
                        float *cov, float *rgb, float *o_raw) {
   const float *p = sc->pos + 3 * (size_t)i;
@@ -338,9 +372,17 @@ void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alp
   float o[ORC_NOUT];
   if (sc->real) {
     /* F4: continuous view direction d_view = v / |v| (three IEEE divisions; 0 at the camera) */
-    float xf[F + 3];
-    for (int k = 0; k < F; ++k) xf[k] = sc->featf[(size_t)i * F + k];
+    float xf[F + 4];
     for (int k = 0; k < 3; ++k) xf[F + k] = (n == 0.0f) ? 0.0f : v[k] / n;
+    xf[F + 3] = n;                               /* R32 distance input (read only when dist_input) */
+    if (sc->bank) {                              /* R32 feature bank */
+      const float y[4] = {xf[F], xf[F + 1], xf[F + 2], n};
+      float w[3];
+      orc_bank_weights(sc, y, w);
+      orc_bank_blend(sc->featf + (size_t)i * F, w, xf);
+    } else {
+      for (int k = 0; k < F; ++k) xf[k] = sc->featf[(size_t)i * F + k];
+    }
     orc_mlp_f32(sc, xf, o);
   } else {
     /* grid path (R3/R6): quantised view direction, exact-integer MLP */

@@ -48,7 +48,12 @@ typedef struct {
    * weights (same shapes as the codes above, any values) and the unquantised view direction */
   int real;
   const float *featf;    /* [N*F] */
-  const float *W1f, *b1f, *W2af, *b2af, *W2cf, *b2cf, *W2sf, *b2sf;
+  const float *W1f, *b1f, *W2af, *b2af, *W2cf, *b2cf, *W2sf, *b2sf;   /* W1f: [F+3+dist_input][3H] */
+  /* R32 (F4, Scaffold-GS combine inputs; real-weights scenes only): dist_input appends the
+   * anchor-camera distance |p_i - p_u| to the MLP input; bank blends the features across strides
+   * 4, 2, 1 with w = softmax(Wb2^T ReLU(Wb1^T (d_view, dist) + bb1) + bb2) */
+  int dist_input, bank;
+  const float *Wb1, *bb1, *Wb2, *bb2;   /* [4][F], [F], [F][3], [3] */
 } orc_scene;
 
 typedef struct {
@@ -116,8 +121,13 @@ float orc_margin(const float *offs_i, const float *s_i);
 int orc_lod_cut(const orc_unified *u, int L, float d0, const float *p);
 int orc_visible(const orc_unified *u, int L, float d0, const float *p, float margin, int level);
 void orc_build_cov(const float q[4], const float S[3], float cov[6]);
-/* F4: the fixed-order fp32 MLP of the real-weights path: x[35] (32 features, d_view) -> o[110] */
-void orc_mlp_f32(const orc_scene *sc, const float x[ORC_F + 3], float o[ORC_NOUT]);
+/* F4: the fixed-order fp32 MLP of the real-weights path: x[35 + dist_input] (32 features, d_view,
+ * [distance]) -> o[110] */
+void orc_mlp_f32(const orc_scene *sc, const float *x, float o[ORC_NOUT]);
+/* R32: the feature bank's softmax weights w[3] (strides 4, 2, 1) for y = (d_view, distance) */
+void orc_bank_weights(const orc_scene *sc, const float y[4], float w[3]);
+/* R32: the blended features fh[k] = w2 f_k + w1 f_{2 (k mod F/2)} + w0 f_{4 (k mod F/4)} (fixed fma order) */
+void orc_bank_blend(const float f[ORC_F], const float w[3], float fh[ORC_F]);
 void orc_derive_anchor(const orc_scene *sc, int i, const float pu[3], float *alpha, float *mu,
                        float *cov, float *rgb, float *o_raw /* [110] or NULL */);
 /* 1 projected, 0 culled, -1 skipped for non-finite parameters (counted) */

@@ -99,6 +99,15 @@ class Scene:
     bbox: np.ndarray = field(default_factory=lambda: np.zeros(6, np.float32))
     # real-weights scene: feat and the decoder weights are fp32 values, not int8 codes
     real: bool = False
+    # F4 Scaffold-GS combine inputs (R32; real-weights scenes only): the anchor-camera distance
+    # as a 36th MLP input (W1 then has F + 4 rows), and the multi-resolution feature bank -- weights
+    # w = softmax(Wb2^T ReLU(Wb1^T (d_view, dist) + bb1) + bb2) blending the features at strides 4, 2, 1
+    dist_input: bool = False
+    bank: bool = False
+    Wb1: np.ndarray = None   # f32 [4, F]
+    bb1: np.ndarray = None   # f32 [F]
+    Wb2: np.ndarray = None   # f32 [F, 3]
+    bb2: np.ndarray = None   # f32 [3]
 
     @property
     def n(self) -> int:
@@ -223,11 +232,16 @@ def make_city_scene(seed: int, n: int, side: float, L: int = 5, width: int = 192
                  L=L, d0=float(np.float32(d0)), bbox=bbox)
 
 
-def with_real_weights(scene: Scene, seed: int = 11) -> Scene:
+def with_real_weights(scene: Scene, seed: int = 11, dist: bool = False, bank: bool = False) -> Scene:
     """F4 input: the same anchors with trained-style fp32 features and decoder
     weights -- continuous values, not on the 2^-7 grid.  Features U(-1, 1); each weight and bias
     uniform in +-(the grid scene's Kaiming code bound)/128 (W1, b1: 21; W2a: 64; b2a and the colour /
-    covariance heads: 22), so activations and opacities spread like the grid scene's."""
+    covariance heads: 22), so activations and opacities spread like the grid scene's.
+
+    dist / bank (R32, Scaffold-GS combine inputs): W1 gains a distance row, U(+-2^-9) per metre so a few
+    hundred metres move a hidden unit by ~0.5; the feature-bank MLP 4 -> F -> 3 has Wb1 U(+-1) on the
+    view direction and U(+-2^-7) on the distance, bb1 U(+-0.25), Wb2 U(+-0.5), bb2 U(+-1): softmax
+    weights that vary with the view, none degenerate."""
     import dataclasses
     n, F, K, H = scene.n, F_DIM, K_GAUSS, H_DIM
 
@@ -235,10 +249,17 @@ def with_real_weights(scene: Scene, seed: int = 11) -> Scene:
         cnt = int(np.prod(shape))
         return ((uniform01(seed, stream, cnt) * 2.0 - 1.0) * (bound / 128.0)).astype(np.float32).reshape(shape)
 
+    W1 = U(31, (F + 3, 3 * H), 21)
+    extra = {}
+    if dist:
+        W1 = np.concatenate([W1, U(39, (1, 3 * H), 0.25)], axis=0)
+    if bank:
+        Wb1 = np.concatenate([U(40, (3, F), 128.0), U(41, (1, F), 1.0)], axis=0)
+        extra = dict(Wb1=Wb1, bb1=U(42, (F,), 32.0), Wb2=U(43, (F, 3), 64.0), bb2=U(44, (3,), 128.0))
     return dataclasses.replace(
-        scene, feat=U(30, (n, F), 128.0), W1=U(31, (F + 3, 3 * H), 21), b1=U(32, (3 * H,), 21),
+        scene, feat=U(30, (n, F), 128.0), W1=W1, b1=U(32, (3 * H,), 21),
         W2a=U(33, (H, K), 64), b2a=U(34, (K,), 22), W2c=U(35, (H, 3 * K), 22), b2c=U(36, (3 * K,), 22),
-        W2s=U(37, (H, 7 * K), 22), b2s=U(38, (7 * K,), 22), real=True)
+        W2s=U(37, (H, 7 * K), 22), b2s=U(38, (7 * K,), 22), real=True, dist_input=dist, bank=bank, **extra)
 
 
 # ----------------------------------------------------------------------------
@@ -342,16 +363,25 @@ def write_gsc2(scene: Scene, path: str) -> None:
     weights : W1 q[(F+3)*3H] | b1 q[3H] | W2a q[H*K] | b2a q[K] | W2c q[H*3K] |
               b2c q[3K] | W2s q[H*7K] | b2s q[7K]
     version 2: q = i8 grid codes (value = code / 128); version 3 (real-weights scenes, F4): q = f32.
+    version 4 (real weights with the R32 combine inputs): after the header a u32 flags word (bit 0:
+    distance input, W1 then has F+4 rows; bit 1: feature bank), and after b2s, with the bank:
+    Wb1 f32[4*F] | bb1 f32[F] | Wb2 f32[F*3] | bb2 f32[3].
     """
     q = "<f4" if scene.real else "i1"
+    v4 = scene.real and (scene.dist_input or scene.bank)
     with open(path, "wb") as fh:
-        fh.write(_HDR.pack(b"GSC2", 3 if scene.real else 2, scene.n, F_DIM, K_GAUSS, scene.L, H_DIM,
-                           scene.d0, *[float(x) for x in scene.bbox]))
-        for a, dt in ((scene.pos, "<f4"), (scene.feat, q), (scene.offs, "<f4"),
-                      (scene.scale, "<f4"), (scene.level, "u1"), (scene.W1, q),
-                      (scene.b1, q), (scene.W2a, q), (scene.b2a, q),
-                      (scene.W2c, q), (scene.b2c, q), (scene.W2s, q),
-                      (scene.b2s, q)):
+        fh.write(_HDR.pack(b"GSC2", 4 if v4 else (3 if scene.real else 2), scene.n, F_DIM, K_GAUSS, scene.L,
+                           H_DIM, scene.d0, *[float(x) for x in scene.bbox]))
+        if v4:
+            fh.write(struct.pack("<I", (1 if scene.dist_input else 0) | (2 if scene.bank else 0)))
+        arrays = [(scene.pos, "<f4"), (scene.feat, q), (scene.offs, "<f4"),
+                  (scene.scale, "<f4"), (scene.level, "u1"), (scene.W1, q),
+                  (scene.b1, q), (scene.W2a, q), (scene.b2a, q),
+                  (scene.W2c, q), (scene.b2c, q), (scene.W2s, q),
+                  (scene.b2s, q)]
+        if v4 and scene.bank:
+            arrays += [(scene.Wb1, "<f4"), (scene.bb1, "<f4"), (scene.Wb2, "<f4"), (scene.bb2, "<f4")]
+        for a, dt in arrays:
             fh.write(np.ascontiguousarray(a, dtype=dt).tobytes())
 
 
@@ -361,10 +391,17 @@ def read_gsc2(path: str) -> Scene:
     if len(data) < _HDR.size:
         raise ValueError(f"GSC2 truncated header at offset {len(data)}")
     magic, ver, n, F, K, L, H, d0, *bbox = _HDR.unpack_from(data, 0)
-    if magic != b"GSC2" or ver not in (2, 3):
+    if magic != b"GSC2" or ver not in (2, 3, 4):
         raise ValueError("GSC2 bad magic/version at offset 0")
-    q = "<f4" if ver == 3 else "i1"
+    q = "<f4" if ver >= 3 else "i1"
     off = _HDR.size
+    flags = 0
+    if ver == 4:
+        if off + 4 > len(data):
+            raise ValueError(f"GSC2 truncated at offset {off}")
+        flags = struct.unpack_from("<I", data, off)[0]
+        off += 4
+    dist, bank = bool(flags & 1), bool(flags & 2)
 
     def take(count, dt, shape):
         nonlocal off
@@ -380,7 +417,7 @@ def read_gsc2(path: str) -> Scene:
     offs = take(n * K * 3, "<f4", (n, K, 3))
     scale = take(n * 3, "<f4", (n, 3))
     level = take(n, "u1", (n,))
-    W1 = take((F + 3) * 3 * H, q, (F + 3, 3 * H))
+    W1 = take((F + 3 + dist) * 3 * H, q, (F + 3 + dist, 3 * H))
     b1 = take(3 * H, q, (3 * H,))
     W2a = take(H * K, q, (H, K))
     b2a = take(K, q, (K,))
@@ -388,9 +425,13 @@ def read_gsc2(path: str) -> Scene:
     b2c = take(3 * K, q, (3 * K,))
     W2s = take(H * 7 * K, q, (H, 7 * K))
     b2s = take(7 * K, q, (7 * K,))
+    extra = {}
+    if bank:
+        extra = dict(Wb1=take(4 * F, "<f4", (4, F)), bb1=take(F, "<f4", (F,)), Wb2=take(F * 3, "<f4", (F, 3)),
+                     bb2=take(3, "<f4", (3,)))
     return Scene(pos=pos, feat=feat, offs=offs, scale=scale, level=level, W1=W1, b1=b1,
-                 W2a=W2a, b2a=b2a, W2c=W2c, b2c=b2c, W2s=W2s, b2s=b2s, L=L, d0=d0, real=ver == 3,
-                 bbox=np.array(bbox, np.float32))
+                 W2a=W2a, b2a=b2a, W2c=W2c, b2c=b2c, W2s=W2s, b2s=b2s, L=L, d0=d0, real=ver >= 3,
+                 dist_input=dist, bank=bank, bbox=np.array(bbox, np.float32), **extra)
 
 
 def write_trajectory(rigs, path: str, fov_y_deg: float, width: int, height: int) -> None:
@@ -430,10 +471,12 @@ class Config:
     near: float = 0.05
     far: float = 5000.0
     real: bool = False     # F4: fp32 non-grid features / decoder weights (with_real_weights)
+    dist: bool = False     # F4 / R32: distance input
+    bank: bool = False     # F4 / R32: feature bank
 
     def scene(self) -> Scene:
         sc = make_city_scene(self.seed, self.n, self.side, self.L, self.width, self.height, self.fov_y_deg)
-        return with_real_weights(sc) if self.real else sc
+        return with_real_weights(sc, dist=self.dist, bank=self.bank) if self.real else sc
 
     @property
     def center(self):
@@ -457,6 +500,10 @@ CONFIGS = {
     "C3R": Config("C3R", 100_000, 130.0, 5, 1920, 1080, 70.0, 10, real=True),
     "C3S": Config("C3S", 100_000, 130.0, 1, 1920, 1080, 70.0, 10, real=True),
     "C4R": Config("C4R", 1_000_000, 400.0, 5, 1920, 1080, 70.0, 10, real=True),
+    # F4 with the Scaffold-GS combine inputs (R32): distance input + feature bank, on C1 / C3 / C3S
+    "C1B": Config("C1B", 1000, 20.0, 3, 64, 64, 70.0, 10, real=True, dist=True, bank=True),
+    "C3B": Config("C3B", 100_000, 130.0, 5, 1920, 1080, 70.0, 10, real=True, dist=True, bank=True),
+    "C3SB": Config("C3SB", 100_000, 130.0, 1, 1920, 1080, 70.0, 10, real=True, dist=True, bank=True),
     # SURVEY §8(f) F3 (depth-policy study): the C3 scene with a street-level head turn whose speed
     # accelerates (C3A: 0.2 -> 40 deg/frame over 300 frames) or changes in stages (C3T: 1 / 10 / 35 deg
     # per frame, 100 frames each) -- the novelty rate then spans 0 -> ~30%, where the guides differ
