@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GSC_ABI_VERSION 2
+#define GSC_ABI_VERSION 3   /* 3: gsc_scene_desc_f32 gained the combine inputs (R32) */
 
 typedef enum {
   GSC_OK = 0,
@@ -137,8 +137,16 @@ typedef struct {
   float d0;
   const float *pos, *feat, *offs, *scale;   /* [N][3], [N][32], [N][10][3], [N][3] */
   const uint8_t *level;                     /* [N] */
-  const float *W1, *b1;                     /* [35][96], [96] */
+  const float *W1, *b1;                     /* [35 + dist_input][96], [96] */
   const float *W2a, *b2a, *W2c, *b2c, *W2s, *b2s;
+  /* Scaffold-GS combine inputs (SURVEY §8(f) F4 "optional distance input / feature bank"; "first
+   * combine operator"; R32 / F4-B), both off when 0:
+   *   dist_input: the anchor-camera distance |p_i - p_u| is the MLP's 36th input (W1 row 35);
+   *   feature_bank: the features enter the MLP blended across strides 4, 2, 1 (every 4th / 2nd value
+   *   tiled back to 32), fh_k = w2 f_k + w1 f_{2 (k mod 16)} + w0 f_{4 (k mod 8)}, with view-dependent
+   *   weights w = softmax(Wb2^T ReLU(Wb1^T (d_view, |p_i - p_u|) + bb1) + bb2). */
+  int32_t dist_input, feature_bank;
+  const float *Wb1, *bb1, *Wb2, *bb2;       /* [4][32], [32], [32][3], [3] (feature_bank only) */
 } gsc_scene_desc_f32;
 
 /* Per-frame record (SPEC FrameRecord S:421-423, CacheStats S:208). */
@@ -183,7 +191,8 @@ int gsc_abi_version(void);
 gsc_status gsc_create(int cuda_device, const gsc_config *cfg, gsc_ctx **out);
 
 /* Load a GSC2 scene file (format in scenegen/__init__.py write_gsc2: version 2 = int8 grid codes,
- * version 3 = fp32 features and weights, the real-weights path F4); resets the cache.
+ * version 3 = fp32 features and weights, the real-weights path F4; version 4 = version 3 with the
+ * combine-input flags word and the feature-bank weights, R32); resets the cache.
  * GSC_EFORMAT with the byte offset on bad magic / truncation / unsupported dims. */
 gsc_status gsc_load_scene(gsc_ctx *ctx, const char *path);
 

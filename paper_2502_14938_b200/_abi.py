@@ -62,7 +62,8 @@ class gsc_scene_desc_f32(C.Structure):
                 ("pos", C.c_void_p), ("feat", C.c_void_p), ("offs", C.c_void_p), ("scale", C.c_void_p),
                 ("level", C.c_void_p), ("W1", C.c_void_p), ("b1", C.c_void_p), ("W2a", C.c_void_p),
                 ("b2a", C.c_void_p), ("W2c", C.c_void_p), ("b2c", C.c_void_p), ("W2s", C.c_void_p),
-                ("b2s", C.c_void_p)]
+                ("b2s", C.c_void_p), ("dist_input", C.c_int32), ("feature_bank", C.c_int32),
+                ("Wb1", C.c_void_p), ("bb1", C.c_void_p), ("Wb2", C.c_void_p), ("bb2", C.c_void_p)]
 
 
 class gsc_frame_stats(C.Structure):
@@ -162,4 +163,14 @@ class SceneDesc:
             a = np.ascontiguousarray(getattr(sc, name), dtype=dt)
             self.keep[name] = a
             setattr(d, name, a.ctypes.data)
+        if self.real:   # R32 combine inputs (distance input, feature bank)
+            d.dist_input = int(bool(getattr(sc, "dist_input", False)))
+            d.feature_bank = int(bool(getattr(sc, "bank", False)))
+            if d.feature_bank:
+                for name in ("Wb1", "bb1", "Wb2", "bb2"):
+                    if getattr(sc, name) is None:   # (passed as NULL: the library rejects it)
+                        continue
+                    a = np.ascontiguousarray(getattr(sc, name), dtype=np.float32)
+                    self.keep[name] = a
+                    setattr(d, name, a.ctypes.data)
         self.desc = d

@@ -39,8 +39,8 @@ void launch_blend(const FrameC &, const uint2 *, const uint32_t *, const uint32_
                   const float2 *, void *, void *, int, FrameCounters *, uint32_t *, bool, bool, int, cudaStream_t);
 void launch_elem(int, const float *, float *, size_t, int, cudaStream_t);
 void launch_derive_f32(const float pu[3], const uint32_t *, const float4 *, const float *, const float *, const float *,
-                       const float *, const float *, const float *, const float *, float *, float4 *, FrameCounters *,
-                       int, cudaStream_t);
+                       const float *, const float *, const float *, const float *, const CombineF32 &, float *, float4 *,
+                       FrameCounters *, int, cudaStream_t);
 int sort_tile_size();
 int emit_tile_size();
 }  // namespace gsc
@@ -89,7 +89,9 @@ struct gsc_ctx {
   DevBuf<int8_t> W1T, W2T;
   DevBuf<int32_t> b1s, b2s;
   bool real = false;                 // real-weights scene (F4): fp32 features / weights below
-  DevBuf<float> featf, W1f, b1f, W2f, b2f;   // [N][32], [35][96], [96], [32][110] (heads concatenated), [110]
+  DevBuf<float> featf, W1f, b1f, W2f, b2f;   // [N][32], [35 + dist][96], [96], [32][110] (heads concatenated), [110]
+  bool dist_input = false, bank = false;      // R32 combine inputs (real-weights scenes)
+  DevBuf<float> Wb1f, bb1f, Wb2f, bb2f;       // feature bank MLP: [4][32], [32], [32][3], [3]
   // cache
   DevBuf<int32_t> birth;
   DevBuf<uint32_t> vis[2];
@@ -297,7 +299,13 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *g, const gsc_
         if (!std::isfinite(p[k])) return false;
       return true;
     };
-    if (!finite(f->feat, (size_t)N * kF) || !finite(f->W1, 35 * 96) || !finite(f->b1, 96) ||
+    if ((f->dist_input != 0 && f->dist_input != 1) || (f->feature_bank != 0 && f->feature_bank != 1) ||
+        (f->feature_bank && (!f->Wb1 || !f->bb1 || !f->Wb2 || !f->bb2)))
+      return fail(ctx, GSC_EINVAL, "invalid combine-input flags or missing feature-bank weights");
+    if (f->feature_bank && (!finite(f->Wb1, 4 * kF) || !finite(f->bb1, kF) || !finite(f->Wb2, kF * 3) ||
+                            !finite(f->bb2, 3)))
+      return fail(ctx, GSC_EFORMAT, "non-finite feature-bank weight");
+    if (!finite(f->feat, (size_t)N * kF) || !finite(f->W1, (size_t)(35 + f->dist_input) * 96) || !finite(f->b1, 96) ||
         !finite(f->W2a, 32 * kK) || !finite(f->b2a, kK) || !finite(f->W2c, 32 * 3 * kK) || !finite(f->b2c, 3 * kK) ||
         !finite(f->W2s, 32 * 7 * kK) || !finite(f->b2s, 7 * kK))
       return fail(ctx, GSC_EFORMAT, "non-finite feature or decoder weight");
@@ -324,7 +332,14 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *g, const gsc_
   CU(ctx->b1s.alloc(g ? 96 : 0));
   CU(ctx->b2s.alloc(g ? kNOut : 0));
   CU(ctx->featf.alloc(f ? (size_t)N * kF : 0));
-  CU(ctx->W1f.alloc(f ? 35 * 96 : 0));
+  const int w1rows = f ? 35 + f->dist_input : 0;
+  ctx->dist_input = f && f->dist_input;
+  ctx->bank = f && f->feature_bank;
+  CU(ctx->W1f.alloc((size_t)w1rows * 96));
+  CU(ctx->Wb1f.alloc(ctx->bank ? 4 * kF : 0));
+  CU(ctx->bb1f.alloc(ctx->bank ? kF : 0));
+  CU(ctx->Wb2f.alloc(ctx->bank ? kF * 3 : 0));
+  CU(ctx->bb2f.alloc(ctx->bank ? 3 : 0));
   CU(ctx->b1f.alloc(f ? 96 : 0));
   CU(ctx->W2f.alloc(f ? 32 * kNOut : 0));
   CU(ctx->b2f.alloc(f ? kNOut : 0));
@@ -343,7 +358,13 @@ static gsc_status upload_scene(gsc_ctx *ctx, const gsc_scene_desc *g, const gsc_
     CU(cudaMemcpy(ctx->b2s.p, b2s.data(), kNOut * 4, cudaMemcpyHostToDevice));
   } else {
     CU(cudaMemcpy(ctx->featf.p, f->feat, (size_t)N * kF * 4, cudaMemcpyHostToDevice));
-    CU(cudaMemcpy(ctx->W1f.p, f->W1, 35 * 96 * 4, cudaMemcpyHostToDevice));
+    CU(cudaMemcpy(ctx->W1f.p, f->W1, (size_t)w1rows * 96 * 4, cudaMemcpyHostToDevice));
+    if (ctx->bank) {
+      CU(cudaMemcpy(ctx->Wb1f.p, f->Wb1, 4 * kF * 4, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->bb1f.p, f->bb1, kF * 4, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->Wb2f.p, f->Wb2, kF * 3 * 4, cudaMemcpyHostToDevice));
+      CU(cudaMemcpy(ctx->bb2f.p, f->bb2, 3 * 4, cudaMemcpyHostToDevice));
+    }
     CU(cudaMemcpy(ctx->b1f.p, f->b1, 96 * 4, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->W2f.p, W2f.data(), W2f.size() * 4, cudaMemcpyHostToDevice));
     CU(cudaMemcpy(ctx->b2f.p, b2f.data(), kNOut * 4, cudaMemcpyHostToDevice));
@@ -442,8 +463,8 @@ static gsc_status load_file(gsc_ctx *ctx, const char *path) {
   if (std::memcmp(buf.data(), "GSC2", 4) != 0) return fail(ctx, GSC_EFORMAT, "bad magic at offset 0");
   uint32_t u[6];
   std::memcpy(u, buf.data() + 4, 24);
-  if (u[0] != 2 && u[0] != 3) return fail(ctx, GSC_EFORMAT, "unsupported version at offset 4");
-  const bool real = u[0] == 3;   // version 3: fp32 features and decoder weights (F4)
+  if (u[0] < 2 || u[0] > 4) return fail(ctx, GSC_EFORMAT, "unsupported version at offset 4");
+  const bool real = u[0] >= 3;   // versions 3, 4: fp32 features and decoder weights (F4)
   const size_t q = real ? 4 : 1;
   const uint32_t N = u[1], F = u[2], K = u[3], L = u[4], H = u[5];
   if (F != (uint32_t)kF || K != (uint32_t)kK || H != (uint32_t)kH)
@@ -451,26 +472,40 @@ static gsc_status load_file(gsc_ctx *ctx, const char *path) {
   float d0;
   std::memcpy(&d0, buf.data() + 28, 4);
   size_t off = hdr;
+  uint32_t flags = 0;   // version 4: bit 0 distance input, bit 1 feature bank (R32)
+  if (u[0] == 4) {
+    if (off + 4 > buf.size()) return fail(ctx, GSC_EFORMAT, "truncated at offset " + std::to_string(off));
+    std::memcpy(&flags, buf.data() + off, 4);
+    off += 4;
+    if (flags > 3) return fail(ctx, GSC_EFORMAT, "unknown flags at offset " + std::to_string(off - 4));
+  }
+  const uint32_t dist = flags & 1u, bank = (flags >> 1) & 1u;
   auto take = [&](size_t bytes, const char *what, const void **ptr) -> bool {
     if (off + bytes > buf.size()) return false;
     *ptr = buf.data() + off;
     off += bytes;
     return true;
   };
-  const void *p[13];
-  const size_t bytes[13] = {N * 12ull, N * 32ull * q, N * 120ull, N * 12ull, N * 1ull, 35 * 96ull * q, 96ull * q,
-                            32 * 10ull * q, 10ull * q, 32 * 30ull * q, 30ull * q, 32 * 70ull * q, 70ull * q};
-  for (int k = 0; k < 13; ++k)
+  const void *p[17];
+  const size_t bytes[17] = {N * 12ull, N * 32ull * q, N * 120ull, N * 12ull, N * 1ull, (35 + dist) * 96ull * q,
+                            96ull * q, 32 * 10ull * q, 10ull * q, 32 * 30ull * q, 30ull * q, 32 * 70ull * q, 70ull * q,
+                            4 * 32ull * 4, 32ull * 4, 32 * 3ull * 4, 3ull * 4};
+  const int narr = bank ? 17 : 13;
+  for (int k = 0; k < narr; ++k)
     if (!take(bytes[k], "", &p[k])) return fail(ctx, GSC_EFORMAT, "truncated at offset " + std::to_string(off));
   // (the file buffer is char-aligned: copy the f32 / int8 arrays through vectors of their type)
   auto fv = [&](int k) { std::vector<float> v(bytes[k] / 4); std::memcpy(v.data(), p[k], bytes[k]); return v; };
   std::vector<float> pos = fv(0), offs = fv(2), scale = fv(3);
   if (real) {
-    std::vector<float> w[13];
+    std::vector<float> w[17];
     for (int k : {1, 5, 6, 7, 8, 9, 10, 11, 12}) w[k] = fv(k);
+    if (bank)
+      for (int k : {13, 14, 15, 16}) w[k] = fv(k);
     gsc_scene_desc_f32 d{(int32_t)N, (int32_t)L, d0, pos.data(), w[1].data(), offs.data(), scale.data(),
                          (const uint8_t *)p[4], w[5].data(), w[6].data(), w[7].data(), w[8].data(), w[9].data(),
-                         w[10].data(), w[11].data(), w[12].data()};
+                         w[10].data(), w[11].data(), w[12].data(), (int32_t)dist, (int32_t)bank,
+                         bank ? w[13].data() : nullptr, bank ? w[14].data() : nullptr,
+                         bank ? w[15].data() : nullptr, bank ? w[16].data() : nullptr};
     return upload_scene(ctx, nullptr, &d);
   }
   gsc_scene_desc d{};
@@ -573,7 +608,10 @@ static gsc_status render(gsc_ctx *ctx, void *out_l, void *out_r, int fmt, cudaSt
   // a3
   if (ctx->real)   // F4: fixed-order fp32 MLP on the CUDA cores
     launch_derive_f32(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->featf.p, ctx->offs.p, ctx->scale.p, ctx->W1f.p,
-                      ctx->b1f.p, ctx->W2f.p, ctx->b2f.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, sA);
+                      ctx->b1f.p, ctx->W2f.p, ctx->b2f.p,
+                      CombineF32{ctx->dist_input ? 1 : 0, ctx->bank ? 1 : 0, ctx->Wb1f.p, ctx->bb1f.p, ctx->Wb2f.p,
+                                 ctx->bb2f.p},
+                      ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms, sA);
   else
     launch_derive(ctx->pu, ctx->misses.p, ctx->pos_m.p, ctx->feat.p, ctx->offs.p, ctx->scale.p, ctx->W1T.p,
                   ctx->b1s.p, ctx->W2T.p, ctx->b2s.p, ctx->alpha.p, ctx->pool.p, ctr, ctx->num_sms,

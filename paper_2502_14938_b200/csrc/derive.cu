@@ -201,6 +201,10 @@ __global__ void __launch_bounds__(kDThreads) derive_kernel(DeriveArgs p) {
 // MMA's accumulation order is not the written one.)  64 anchors per CTA iteration: layer 1 as
 // 64 x 96 outputs (thread = (anchor, hidden unit), weights W1[k][n] read conflict-free across n,
 // inputs broadcast), layer 2 as 64 x 110 outputs, then the shared epilogue (derive_gaussian).
+// R32 combine inputs (kDist / kBank, F4-B; "first combine operator"): the distance
+// |p_i - p_u| as the 36th input, and the feature bank -- one thread per anchor evaluates the bank MLP
+// (4 -> 32 -> 3, softmax), then the blended features fh_k = fma(w2, f_k, fma(w1, f_{2 (k mod 16)},
+// w0 f_{4 (k mod 8)})) are formed in SMEM by index arithmetic (no copies of the feature rows).
 struct DeriveF32Args {
   float pu0, pu1, pu2;
   const uint32_t *misses;
@@ -211,6 +215,7 @@ struct DeriveF32Args {
   const float *b1;       // [96]
   const float *W2;       // [32][110] (heads side by side: alpha 0..9 | colour 10..39 | covariance 40..109)
   const float *b2;       // [110]
+  CombineF32 cmb;
   float *alpha;
   float4 *pool;
   FrameCounters *ctr;
@@ -219,22 +224,33 @@ struct DeriveF32Args {
 constexpr int kFA = 64;   // anchors per CTA iteration
 
 struct DeriveF32Smem {
-  float W1[kF + 3][96];
+  float W1[kF + 4][96];      // (row kF + 3: the distance input, R32)
   float b1[96];
   float W2[kH][kNOut];
   float b2[kNOut];
-  float x[kFA][kF + 4];      // inputs (32 features, d_view; padded row)
+  float Wb1[4][kF], bb1[kF], Wb2[kF][3], bb2[3];   // R32 feature bank
+  float x[kFA][kF + 4];      // inputs (32 features, d_view, distance)
+  float fr[kFA][kF + 1];     // raw features (feature bank)
+  float wb[kFA][3];          // bank weights
   float hid[kFA][96 + 1];
   float o[kFA][kNOut + 1];
   uint32_t anchor[kFA];
   uint32_t base;
 };
 
+template <bool kDist, bool kBank>
 __global__ void __launch_bounds__(kDThreads) derive_f32_kernel(DeriveF32Args p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   DeriveF32Smem &S = *reinterpret_cast<DeriveF32Smem *>(smem_raw);
   const int t = threadIdx.x;
-  for (int w = t; w < (kF + 3) * 96; w += kDThreads) (&S.W1[0][0])[w] = p.W1[w];
+  constexpr int kNin = kF + 3 + (kDist ? 1 : 0);
+  for (int w = t; w < kNin * 96; w += kDThreads) (&S.W1[0][0])[w] = p.W1[w];
+  if (kBank) {
+    for (int w = t; w < 4 * kF; w += kDThreads) (&S.Wb1[0][0])[w] = p.cmb.Wb1[w];
+    for (int w = t; w < kF * 3; w += kDThreads) (&S.Wb2[0][0])[w] = p.cmb.Wb2[w];
+    for (int w = t; w < kF; w += kDThreads) S.bb1[w] = p.cmb.bb1[w];
+    for (int w = t; w < 3; w += kDThreads) S.bb2[w] = p.cmb.bb2[w];
+  }
   for (int w = t; w < 96; w += kDThreads) S.b1[w] = p.b1[w];
   for (int w = t; w < kH * kNOut; w += kDThreads) (&S.W2[0][0])[w] = p.W2[w];
   for (int w = t; w < kNOut; w += kDThreads) S.b2[w] = p.b2[w];
@@ -252,22 +268,58 @@ __global__ void __launch_bounds__(kDThreads) derive_f32_kernel(DeriveF32Args p) 
       const float4 pm = p.pos_m[i];
       const float v0 = __fsub_rn(pm.x, p.pu0), v1 = __fsub_rn(pm.y, p.pu1), v2 = __fsub_rn(pm.z, p.pu2);
       const float n = __fsqrt_rn(__fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)), __fmul_rn(v2, v2)));
-      S.x[t][kF + 0] = n == 0.0f ? 0.0f : __fdiv_rn(v0, n);
-      S.x[t][kF + 1] = n == 0.0f ? 0.0f : __fdiv_rn(v1, n);
-      S.x[t][kF + 2] = n == 0.0f ? 0.0f : __fdiv_rn(v2, n);
+      const float d0 = n == 0.0f ? 0.0f : __fdiv_rn(v0, n);
+      const float d1 = n == 0.0f ? 0.0f : __fdiv_rn(v1, n);
+      const float d2 = n == 0.0f ? 0.0f : __fdiv_rn(v2, n);
+      S.x[t][kF + 0] = d0;
+      S.x[t][kF + 1] = d1;
+      S.x[t][kF + 2] = d2;
+      S.x[t][kF + 3] = n;   // R32 distance input (read by layer 1 only with kDist)
+      if (kBank) {
+        // bank MLP (R32, the oracle's orc_bank_weights order): h = ReLU(bb1 + Wb1^T y), z = bb2 + Wb2^T h,
+        // w = softmax(z) with the max subtracted
+        const float y[4] = {d0, d1, d2, n};
+        float z0 = S.bb2[0], z1 = S.bb2[1], z2 = S.bb2[2];
+#pragma unroll 4
+        for (int c = 0; c < kF; ++c) {
+          float acc = S.bb1[c];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) acc = __fmaf_rn(S.Wb1[k][c], y[k], acc);
+          const float h = acc > 0.0f ? acc : 0.0f;
+          z0 = __fmaf_rn(S.Wb2[c][0], h, z0);
+          z1 = __fmaf_rn(S.Wb2[c][1], h, z1);
+          z2 = __fmaf_rn(S.Wb2[c][2], h, z2);
+        }
+        const float zm = fmaxf(fmaxf(z0, z1), z2);
+        const float e0 = exp_s(__fsub_rn(z0, zm)), e1 = exp_s(__fsub_rn(z1, zm)), e2 = exp_s(__fsub_rn(z2, zm));
+        const float sum = __fadd_rn(__fadd_rn(e0, e1), e2);
+        S.wb[t][0] = __fdiv_rn(e0, sum);
+        S.wb[t][1] = __fdiv_rn(e1, sum);
+        S.wb[t][2] = __fdiv_rn(e2, sum);
+      }
     }
     for (int w = t; w < kFA * (kF / 4); w += kDThreads) {   // features: one float4 per thread
       const int a = w / (kF / 4), c4 = w % (kF / 4);
       const float4 f = a < na ? reinterpret_cast<const float4 *>(p.feat)[(size_t)p.misses[base + a] * (kF / 4) + c4]
                               : make_float4(0.f, 0.f, 0.f, 0.f);
-      S.x[a][4 * c4 + 0] = f.x; S.x[a][4 * c4 + 1] = f.y; S.x[a][4 * c4 + 2] = f.z; S.x[a][4 * c4 + 3] = f.w;
+      float *dst = kBank ? &S.fr[a][4 * c4] : &S.x[a][4 * c4];
+      dst[0] = f.x; dst[1] = f.y; dst[2] = f.z; dst[3] = f.w;
     }
     __syncthreads();
+    if (kBank) {   // blended features (strides 4, 2, 1), fixed fma order
+      for (int w = t; w < kFA * kF; w += kDThreads) {
+        const int a = w / kF, k = w % kF;
+        const float *fr = S.fr[a];
+        S.x[a][k] = __fmaf_rn(S.wb[a][2], fr[k], __fmaf_rn(S.wb[a][1], fr[2 * (k % (kF / 2))],
+                                                           __fmul_rn(S.wb[a][0], fr[4 * (k % (kF / 4))])));
+      }
+      __syncthreads();
+    }
     for (int o = t; o < kFA * 96; o += kDThreads) {
       const int a = o / 96, n = o - a * 96;
       float acc = S.b1[n];
 #pragma unroll
-      for (int k = 0; k < kF + 3; ++k) acc = __fmaf_rn(S.W1[k][n], S.x[a][k], acc);
+      for (int k = 0; k < kNin; ++k) acc = __fmaf_rn(S.W1[k][n], S.x[a][k], acc);
       S.hid[a][n] = acc > 0.0f ? acc : 0.0f;   // ReLU
     }
     __syncthreads();
@@ -546,16 +598,23 @@ static PerDevice<int> g_mma_grid, g_derive_grid, g_f32_grid;
 
 void launch_derive_f32(const float pu[3], const uint32_t *misses, const float4 *pos_m, const float *feat,
                        const float *offs, const float *scale, const float *W1, const float *b1, const float *W2,
-                       const float *b2, float *alpha, float4 *pool, FrameCounters *ctr, int num_sms, cudaStream_t st) {
-  DeriveF32Args a{pu[0], pu[1], pu[2], misses, pos_m, feat, offs, scale, W1, b1, W2, b2, alpha, pool, ctr};
+                       const float *b2, const CombineF32 &cmb, float *alpha, float4 *pool, FrameCounters *ctr,
+                       int num_sms, cudaStream_t st) {
+  DeriveF32Args a{pu[0], pu[1], pu[2], misses, pos_m, feat, offs, scale, W1, b1, W2, b2, cmb, alpha, pool, ctr};
   const int smem = (int)sizeof(DeriveF32Smem);
   const int grid = g_f32_grid.get([&](int &grid) {
-    cudaFuncSetAttribute(derive_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(derive_f32_kernel<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(derive_f32_kernel<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(derive_f32_kernel<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaFuncSetAttribute(derive_f32_kernel<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, derive_f32_kernel, kDThreads, smem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, derive_f32_kernel<true, true>, kDThreads, smem);
     grid = num_sms * (per_sm > 0 ? per_sm : 1);
   });
-  derive_f32_kernel<<<grid, kDThreads, smem, st>>>(a);
+  if (cmb.dist && cmb.bank) derive_f32_kernel<true, true><<<grid, kDThreads, smem, st>>>(a);
+  else if (cmb.dist) derive_f32_kernel<true, false><<<grid, kDThreads, smem, st>>>(a);
+  else if (cmb.bank) derive_f32_kernel<false, true><<<grid, kDThreads, smem, st>>>(a);
+  else derive_f32_kernel<false, false><<<grid, kDThreads, smem, st>>>(a);
 }
 
 void launch_derive(const float pu[3], const uint32_t *misses, const float4 *pos_m, const int8_t *feat,

@@ -82,6 +82,12 @@ struct SplatBufs {
   uint32_t list_cap;
 };
 
+// R32 combine inputs of the real-weights derivation (F4-B)
+struct CombineF32 {
+  int dist, bank;                        // distance input, feature bank
+  const float *Wb1, *bb1, *Wb2, *bb2;    // bank MLP [4][32], [32], [32][3], [3]
+};
+
 struct EmitIn {
   const uint32_t *sorted;    // splat indices in depth order
   const uint32_t *count;     // kept tiles per splat

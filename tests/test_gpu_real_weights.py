@@ -143,3 +143,111 @@ def test_c4r_real_weights_full_size(orc):
     for f in range(6):
         st, _ = _frame(o, r, traj[f], full=f in (0, 5))
         assert not st["overflow"]
+
+
+# ---- R32 combine inputs (SURVEY §8(f) F4 "optional distance input / feature bank")
+@pytest.mark.parametrize("dist,bank", [(True, False), (False, True), (True, True)])
+def test_c1_combine_inputs_all_poses(orc, dist, bank):
+    """Distance input and / or feature bank on the C1 scene: derived pool, splats, sorted keys bit-exact
+    against the oracle's orc_bank_weights / orc_bank_blend / orc_mlp_f32 chain, pixels within tolerance."""
+    cfg = sg.config("C1R")
+    sc = sg.with_real_weights(sg.config("C1").scene(), dist=dist, bank=bank)
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    for rig in sg.trajectory(cfg):
+        _frame(o, r, rig, True)
+
+
+def test_c1b_moving_cache(orc):
+    cfg = sg.config("C1B")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg, d_max=4))
+    r = renderer(cfg, d_max=4).load(sc)
+    c = cfg.center
+    for f in range(16):
+        eye = c + np.array([25 * np.cos(0.12 * f), 25 * np.sin(0.12 * f), 2.0 + 0.5 * f])
+        _frame(o, r, sg.look_at_rig(eye, c + np.array([0, 0, 3.0]), 0.064), full=f % 4 == 0)
+
+
+def test_c3b_trajectory(orc):
+    """100k anchors, 2K binocular, distance input + feature bank: the first 11 frames of the C3 orbit,
+    full parity at frames 0 (cold) and 10 (the flush)."""
+    cfg = sg.config("C3B")
+    sc = cfg.scene()
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    for f in range(11):
+        st, _ = _frame(o, r, traj[f], full=f in (0, 10))
+        assert not st["overflow"]
+
+
+def test_c3sb_scaffold_no_lod(orc):
+    """The Scaffold-GS configuration the combine inputs come from: L = 1 (no LoD), distance input and
+    feature bank; frames 0 and 150 of the C3 orbit fully bit-exact."""
+    cfg = sg.config("C3SB")
+    sc = cfg.scene()
+    assert sc.L == 1 and sc.dist_input and sc.bank
+    o = orc.Oracle(sc, oracle_config(orc, cfg))
+    r = renderer(cfg).load(sc)
+    traj = sg.trajectory(cfg)
+    _frame(o, r, traj[0], True)
+    o.reset()
+    r.reset_cache()
+    _frame(o, r, traj[150], True)
+
+
+def test_gsc2_v4_file(orc, tmp_path):
+    """GSC2 version 4 (combine-input flags + feature-bank weights) through gsc_load_scene equals the
+    host-array load, for each combination of the two inputs."""
+    cfg = sg.config("C1R")
+    for dist, bank in ((True, False), (False, True), (True, True)):
+        sc = sg.with_real_weights(sg.config("C1").scene(), dist=dist, bank=bank)
+        path = str(tmp_path / f"c1_{int(dist)}{int(bank)}.gsc2")
+        sg.write_gsc2(sc, path)
+        rf = renderer(cfg).load(path)
+        rh = renderer(cfg).load(sc)
+        for rig in sg.trajectory(cfg):
+            fl, _, _ = rf.render(rig)
+            hl, _, _ = rh.render(rig)
+            assert np.array_equal(rf.debug("pool"), rh.debug("pool"))
+            assert np.array_equal(fl.cpu().numpy(), hl.cpu().numpy())
+
+
+def test_combine_input_errors(tmp_path):
+    """Feature bank without its weights -> GSC_EINVAL; a non-finite bank weight -> GSC_EFORMAT; a v4 file
+    cut inside the bank weights -> GSC_EFORMAT naming the offset; unknown flag bits -> GSC_EFORMAT."""
+    import copy
+    import re
+    import struct
+    from paper_2502_14938_b200 import _abi
+    cfg = sg.config("C1R")
+    sc = sg.with_real_weights(sg.config("C1").scene(), dist=True, bank=True)
+    bad = copy.copy(sc)
+    bad.Wb2 = None
+    with pytest.raises(_abi.GscError) as ei:
+        renderer(cfg).load(bad)
+    assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EINVAL"
+    bad = copy.copy(sc)
+    bad.bb1 = sc.bb1.copy()
+    bad.bb1[5] = np.inf
+    with pytest.raises(_abi.GscError) as ei:
+        renderer(cfg).load(bad)
+    assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
+    path = str(tmp_path / "b.gsc2")
+    sg.write_gsc2(sc, path)
+    data = open(path, "rb").read()
+    cut = str(tmp_path / "cut.gsc2")
+    bank_bytes = (4 * 32 + 32 + 32 * 3 + 3) * 4
+    with open(cut, "wb") as fh:
+        fh.write(data[:len(data) - bank_bytes + 100])
+    with pytest.raises(_abi.GscError) as ei:
+        renderer(cfg).load(cut)
+    assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
+    assert int(re.search(r"offset (\d+)", str(ei.value)).group(1)) == len(data) - bank_bytes
+    flags = str(tmp_path / "flags.gsc2")
+    with open(flags, "wb") as fh:
+        fh.write(data[:56] + struct.pack("<I", 4) + data[60:])
+    with pytest.raises(_abi.GscError) as ei:
+        renderer(cfg).load(flags)
+    assert _abi.STATUS_NAMES[ei.value.status] == "GSC_EFORMAT"
