@@ -77,6 +77,32 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 constexpr int kBWarps = kBThreads / 32;
 
+
+// Packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2: two IEEE fp32 operations per instruction, each
+// element rounded exactly as the scalar __fadd_rn / __fmul_rn / __fmaf_rn; a scalar operand is broadcast
+// by the hardware, so a splat-pair or pixel constant costs no move).
+struct f2p { unsigned long long r; };
+__device__ __forceinline__ f2p pk2(float a, float b) {
+  f2p o; asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b)); return o;
+}
+__device__ __forceinline__ void up2(f2p x, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.r));
+}
+__device__ __forceinline__ f2p add2(f2p a, f2p b) { f2p o; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
+__device__ __forceinline__ f2p mul2(f2p a, f2p b) { f2p o; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
+__device__ __forceinline__ f2p fma2(f2p a, f2p b, f2p c) {
+  f2p o; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r)); return o;
+}
+__device__ __forceinline__ f2p bc2(float a) { return pk2(a, a); }
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d; asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c)); return d;
+}
+__device__ __forceinline__ float fminabs3(float a, float b, float c) {   // min(a, |b|, |c|)
+  float d; asm("min.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(fabsf(b)), "f"(fabsf(c))); return d;
+}
+__device__ __forceinline__ float set_ge(float a, float b) {   // 1.0f if a >= b else 0.0f
+  float d; asm("set.ge.f32.f32 %0, %1, %2;" : "=f"(d) : "f"(a), "f"(b)); return d;
+}
 __device__ __forceinline__ float4 lds_f4(uint32_t a) {
   float4 v;
   asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
@@ -87,6 +113,16 @@ __device__ __forceinline__ float2 lds_f2(uint32_t a) {
   asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
   return v;
 }
+__device__ __forceinline__ void sts_f(uint32_t a, float x) { asm volatile("st.shared.f32 [%0], %1;" :: "r"(a), "f"(x)); }
+__device__ __forceinline__ void sts_f2(uint32_t a, float x, float y) {
+  asm volatile("st.shared.v2.f32 [%0], {%1, %2};" :: "r"(a), "f"(x), "f"(y));
+}
+
+// Per-warp staging planes: the block's splats in pair groups (slots 2k, 2k+1), so that one 16-byte load
+// gives a field of both splats of a group, ready for the packed instructions:
+//   P0 (u0 u1 v0 v1)  P1 (a'0 a'1 b'0 b'1)  P2 (c'0 c'1 alpha0 alpha1)  P3 (g0 b0 g1 b1)  P4 (r0 r1)
+constexpr uint32_t kPl = 16 * 16;              // bytes per float4 plane (16 pair groups)
+constexpr uint32_t kWarpStage = 4 * kPl + 16 * 8;   // + P4 (float2 per group) = 1152 bytes
 
 template <bool kCount>   // kCount: accumulate n_evals / n_exp (GSC_F_COUNT_EVALS)
 __global__ void __launch_bounds__(kBThreads)
@@ -95,9 +131,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
              const float4 *__restrict__ spA, const float4 *__restrict__ spB, const float2 *__restrict__ spC,
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr,
              uint32_t *__restrict__ fixup) {
-  // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
-  // walks all three (offsets 0, 512, 1024 bytes)
-  __shared__ float4 slots[kBWarps][96];
+  __shared__ __align__(16) unsigned char stage[kBWarps * kWarpStage];
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
@@ -114,17 +148,21 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   uint2 rg = make_uint2(~ranges[tile].x, ranges[tile].y);
   rg.x = __shfl_sync(0xFFFFFFFFu, rg.x, 0);   // (uniform by construction; tells the compiler)
   rg.y = __shfl_sync(0xFFFFFFFFu, rg.y, 0);
-  float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
+  float T = 1.0f, C0 = 0.0f;
+  f2p C12 = pk2(0.0f, 0.0f);
   // bias of the exponent: 0 while the lane composites, -1000 once it has terminated (or lies outside
   // the image): ex2 then returns 0, so nothing is accepted any more (no predicate on the hot path)
   float bias = inside ? 0.0f : -1000.0f;
+  // Fast-path threshold: a splat pair whose T' stays >= thr can flip no stop decision (T' >= 1e-4 +
+  // kTBand) and needs none of the stop bookkeeping; below it (or once T sits inside the band: thr = T,
+  // so only an accepted splat reaches it) the pair is replayed by the warp's exact step-by-step path.
+  float thr = inside ? 0.0001f + kTBand : -1.0f;
   float trej = 1.0f;        // T' of the splat the lane stopped before (1: not stopped)
-  float wl = 0.0f;          // contribution alpha' T of the lane's last accepted splat
+  float wl = 0.0f;          // contribution alpha' T of the last accepted splat of a slow-path pair
   float amarg = 1.0f;       // min over the lane's evaluations of |alpha' - 1/255|
   float xmax = -1.0f;       // max of the exponent argument: > 0 iff some evaluation had power > 0
   uint32_t nev = 0, nexp = 0;
-  uint32_t base = (uint32_t)__cvta_generic_to_shared(&slots[warp][0]);
-  asm volatile("" : "+r"(base));   // keep the slot address in a register
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage + warp * kWarpStage);
   const uint32_t lt = lanemask_lt();
 
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
@@ -133,58 +171,107 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     // the pair key's block mask (bit = warp) says whether the splat's box of {power >= skip bound}
     // meets this warp's 8x4 block (computed by project.cu with the fp32 test of DESIGN.md N5)
     const bool in = idx < rg.y && ((pair_keys[idx] >> (24 + warp)) & 1u);
-    // compact the block's splats into the warp's slots, depth order preserved
+    // compact the block's splats into the warp's pair-group planes, depth order preserved
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
+    const uint32_t n = __popc(bits);
     if (in) {
       const uint32_t c = pair_vals[idx];
       const uint32_t slot = __popc(bits & lt);
-      slots[warp][slot] = spA[c];
-      slots[warp][32 + slot] = spB[c];
-      *reinterpret_cast<float2 *>(&slots[warp][64 + slot]) = spC[c];
+      const float4 A = spA[c], B = spB[c];
+      const float2 Cc = spC[c];
+      const uint32_t s = base + (slot >> 1) * 16 + (slot & 1) * 4;
+      sts_f(s, A.x);
+      sts_f(s + 8, A.y);
+      sts_f(s + kPl, A.z);
+      sts_f(s + kPl + 8, A.w);
+      sts_f(s + 2 * kPl, B.x);
+      sts_f(s + 2 * kPl + 8, B.z);
+      sts_f2(base + 3 * kPl + (slot >> 1) * 16 + (slot & 1) * 8, Cc.x, Cc.y);
+      sts_f(base + 4 * kPl + (slot >> 1) * 8 + (slot & 1) * 4, B.w);
     }
-    const uint32_t n = __popc(bits);
+    if ((n & 1u) && lane == 0) {   // odd count: a zero splat (alpha 0: never accepted, guards quiet) in slot n
+      const uint32_t s = base + (n >> 1) * 16 + 4;
+      sts_f(s, 0.0f); sts_f(s + 8, 0.0f);
+      sts_f(s + kPl, 0.0f); sts_f(s + kPl + 8, 0.0f);
+      sts_f(s + 2 * kPl, 0.0f); sts_f(s + 2 * kPl + 8, 0.0f);
+      sts_f2(base + 3 * kPl + (n >> 1) * 16 + 8, 0.0f, 0.0f);
+      sts_f(base + 4 * kPl + (n >> 1) * 8 + 4, 0.0f);
+    }
     __syncwarp();
-    const uint32_t end = base + 16 * n;
+    const uint32_t ng = (n + 1) >> 1;
     const bool done0 = bias < 0.0f;
-    uint32_t pstop = end;
-#pragma unroll 4
-    for (uint32_t j = 0; j < n; ++j) {   // warp-uniform trip count, no divergent branch
-      const uint32_t p = base + 16 * j;
-      const float4 a = lds_f4(p);          // (u, v, a' = -A/2, b' = -B)
-      const float4 q = lds_f4(p + 512);    // (c' = -C/2, skip bound, alpha, r)
-      const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
-      const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
-      const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));   // N6, the oracle's bits
-      const float x = __fmaf_rn(power, kLog2e, bias);   // > 0 iff power > 0 while the lane composites
-      xmax = fmaxf(xmax, x);               // (3DGS skips power > 0: left to the exact replay)
-      float al = fminf(0.99f, __fmul_rn(q.z, ex2_approx(x)));
-      amarg = fminf(amarg, fabsf(__fsub_rn(al, kAlphaMin)));
-      al = al >= kAlphaMin ? al : 0.0f;
-      const float Tn = __fmaf_rn(-al, T, T);
-      const bool term = Tn < 0.0001f;      // stop before this splat; the rest is not evaluated
-      if (kCount) {
-        nexp += al > 0.0f && !term;
-        if (term && bias == 0.0f) pstop = p;
+    uint32_t jstop = n;     // (kCount) index of the splat the lane stopped before
+#pragma unroll 2
+    for (uint32_t g = 0; g < ng; ++g) {   // warp-uniform trip count, no divergent branch on the fast path
+      const uint32_t p = base + 16 * g;
+      const float4 P0 = lds_f4(p);                 // u0 u1 v0 v1
+      const float4 P1 = lds_f4(p + kPl);           // a'0 a'1 b'0 b'1
+      const float4 P2 = lds_f4(p + 2 * kPl);       // c'0 c'1 alpha0 alpha1
+      const f2p dx = add2(pk2(P0.x, P0.y), bc2(-pxc));          // fl(u - pxc): adding -pxc is subtracting
+      const f2p dy = add2(pk2(P0.z, P0.w), bc2(-pyc));
+      const f2p qq = fma2(pk2(P1.x, P1.y), dx, mul2(pk2(P1.z, P1.w), dy));
+      const f2p pw = fma2(dx, qq, mul2(mul2(pk2(P2.x, P2.y), dy), dy));   // N6, the oracle's bits
+      float x0, x1;
+      up2(fma2(pw, bc2(kLog2e), bc2(bias)), x0, x1);   // > 0 iff power > 0 while the lane composites
+      xmax = fmax3(xmax, x0, x1);                       // (3DGS skips power > 0: left to the exact replay)
+      f2p al = mul2(pk2(P2.z, P2.w), pk2(ex2_approx(x0), ex2_approx(x1)));
+      float a0, a1;
+      up2(al, a0, a1);
+      a0 = fminf(0.99f, a0);
+      a1 = fminf(0.99f, a1);
+      float d0, d1;
+      up2(add2(pk2(a0, a1), bc2(-kAlphaMin)), d0, d1);
+      amarg = fminabs3(amarg, d0, d1);
+      up2(mul2(pk2(a0, a1), pk2(set_ge(a0, kAlphaMin), set_ge(a1, kAlphaMin))), a0, a1);   // skip: alpha' = 0
+      const float Tn0 = __fmaf_rn(-a0, T, T);
+      const float Tn1 = __fmaf_rn(-a1, Tn0, Tn0);
+      float w0, w1;
+      if (__any_sync(0xFFFFFFFFu, Tn1 < thr)) {
+        // slow path (rare: a stop, or T' near the stop threshold): the step-by-step decisions with the
+        // bookkeeping the exactness guards need
+        float wk[2];
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const float ak = k ? a1 : a0;
+          const float Tn = __fmaf_rn(-ak, T, T);
+          const bool term = Tn < 0.0001f && bias == 0.0f;   // stop before this splat
+          if (kCount) {
+            nexp += ak > 0.0f && !term && bias == 0.0f;
+            if (term) jstop = 2 * g + k;
+          }
+          trej = term ? Tn : trej;
+          const float w = (term || bias != 0.0f) ? 0.0f : __fmul_rn(ak, T);
+          bias = term ? -1000.0f : bias;
+          wl = w > 0.0f ? w : wl;
+          T = w > 0.0f ? Tn : T;
+          wk[k] = w;
+        }
+        w0 = wk[0];
+        w1 = wk[1];
+        thr = fminf(thr, T);
+      } else {
+        if (kCount) nexp += (a0 > 0.0f) + (a1 > 0.0f);
+        w0 = __fmul_rn(a0, T);
+        w1 = __fmul_rn(a1, Tn0);
+        T = Tn1;
       }
-      trej = term ? Tn : trej;
-      bias = term ? -1000.0f : bias;
-      const float w = term ? 0.0f : __fmul_rn(al, T);
-      wl = w > 0.0f ? w : wl;
-      const float2 gb = lds_f2(p + 1024);
-      C0 = __fmaf_rn(q.w, w, C0);
-      C1 = __fmaf_rn(gb.x, w, C1);
-      C2 = __fmaf_rn(gb.y, w, C2);
-      T = term ? T : Tn;
+      const float4 P3 = lds_f4(p + 3 * kPl);               // g0 b0 g1 b1
+      const float2 P4 = lds_f2(base + 4 * kPl + 8 * g);    // r0 r1
+      C0 = __fmaf_rn(P4.x, w0, C0);
+      C0 = __fmaf_rn(P4.y, w1, C0);
+      C12 = fma2(pk2(P3.x, P3.y), bc2(w0), C12);
+      C12 = fma2(pk2(P3.z, P3.w), bc2(w1), C12);
     }
-    if (kCount && !done0) nev += (pstop - base) / 16 + (pstop != end ? 1 : 0);
+    if (kCount && !done0) nev += jstop + (jstop != n ? 1 : 0);
     __syncwarp();
   }
   // R5 exactness check: the fast exponential can flip a decision only (i) where alpha' came within
   // 2^-19 relative of 1/255 (skip), (ii) where power > 0 (skip), (iii) where T' came within kTBand of
-  // 1e-4 (stop) -- for the splat the lane stopped before (trej) or its last accepted one (T) -- and a
-  // stop flip matters only if that splat's contribution exceeds kJump.  Such pixels (rare) go to the
-  // exact replay (blend_fixup_kernel: the oracle's op sequence with exp_s); everywhere else every
-  // decision is the oracle's.
+  // 1e-4 (stop) -- for the splat the lane stopped before (trej) or its last accepted one (T; a splat
+  // accepted by the fast path leaves T' >= 1e-4 + kTBand, so only a slow-path one can end in the band)
+  // -- and a stop flip matters only if that splat's contribution exceeds kJump.  Such pixels (rare) go
+  // to the exact replay (blend_fixup_kernel: the oracle's op sequence with exp_s); everywhere else
+  // every decision is the oracle's.
   const bool redo = inside && (xmax > 0.0f || amarg <= kAlphaGuard ||
                                (fabsf(__fsub_rn(T, 0.0001f)) <= kTBand && wl > kJump) ||
                                (fabsf(__fsub_rn(trej, 0.0001f)) <= kTBand && __fsub_rn(T, trej) > kJump));
@@ -207,6 +294,8 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     }
   }
   if (!inside || redo) return;
+  float C1, C2;
+  up2(C12, C1, C2);
   write_pixel(fc, e, px, py, T, C0, C1, C2, out_l, out_r, fmt);
 }
 
