@@ -41,7 +41,7 @@
 extern "C" {
 #endif
 
-#define GSC_ABI_VERSION 3   /* 3: gsc_scene_desc_f32 gained the combine inputs (R32) */
+#define GSC_ABI_VERSION 4   /* 3: gsc_scene_desc_f32 gained the combine inputs (R32); 4: gsc_frame_stats.n_evals_list */
 
 typedef enum {
   GSC_OK = 0,
@@ -167,6 +167,12 @@ typedef struct {
                                                     centre (skip the splat, count it) */
   uint32_t n_blend_fixup;                        /* pixels the blend re-ran with the exact exp_s because a decision
                                                     came within the fast exponential's error band (R5) */
+  uint64_t n_evals_list;                         /* blend: the method's (pixel, splat) evaluations -- per pixel, the
+                                                    entries of its tile's sorted list up to and including the one it
+                                                    stopped before, all of them if it never stopped (Eq. 1 over the
+                                                    tile list; the oracle's orc_blend_pixel count, SURVEY
+                                                    d-3); n_evals counts what the kernel executed after its
+                                                    decision-preserving 8x4-block skip (GSC_F_COUNT_EVALS) */
 } gsc_frame_stats;
 
 /* out formats */

@@ -75,7 +75,7 @@ class gsc_frame_stats(C.Structure):
                 ("ms_depth_sort", C.c_float), ("ms_emit", C.c_float), ("ms_tile_sort", C.c_float),
                 ("ms_ranges", C.c_float), ("ms_blend", C.c_float), ("ms_total", C.c_float),
                 ("n_evals", C.c_uint64), ("n_exp", C.c_uint64), ("n_nonfinite_skipped", C.c_uint32),
-                ("n_blend_fixup", C.c_uint32)]
+                ("n_blend_fixup", C.c_uint32), ("n_evals_list", C.c_uint64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -132,6 +132,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
              void *__restrict__ out_l, void *__restrict__ out_r, int fmt, FrameCounters *__restrict__ ctr,
              uint32_t *__restrict__ fixup) {
   __shared__ __align__(16) unsigned char stage[kBWarps * kWarpStage];
+  __shared__ uint32_t s_idx[kCount ? kBWarps * 32 : 1];   // (kCount) list index of each staged splat
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
@@ -161,7 +162,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   float wl = 0.0f;          // contribution alpha' T of the last accepted splat of a slow-path pair
   float amarg = 1.0f;       // min over the lane's evaluations of |alpha' - 1/255|
   float xmax = -1.0f;       // max of the exponent argument: > 0 iff some evaluation had power > 0
-  uint32_t nev = 0, nexp = 0;
+  uint32_t nev = 0, nexp = 0, lstop = 0;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage + warp * kWarpStage);
   const uint32_t lt = lanemask_lt();
 
@@ -177,6 +178,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     if (in) {
       const uint32_t c = pair_vals[idx];
       const uint32_t slot = __popc(bits & lt);
+      if (kCount) s_idx[warp * 32 + slot] = idx;
       const float4 A = spA[c], B = spB[c];
       const float2 Cc = spC[c];
       const uint32_t s = base + (slot >> 1) * 16 + (slot & 1) * 4;
@@ -237,7 +239,10 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
           const bool term = Tn < 0.0001f && bias == 0.0f;   // stop before this splat
           if (kCount) {
             nexp += ak > 0.0f && !term && bias == 0.0f;
-            if (term) jstop = 2 * g + k;
+            if (term) {
+              jstop = 2 * g + k;
+              lstop = s_idx[warp * 32 + 2 * g + k];
+            }
           }
           trej = term ? Tn : trej;
           const float w = (term || bias != 0.0f) ? 0.0f : __fmul_rn(ak, T);
@@ -283,14 +288,19 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     if (redo) fixup[at + __popc(rb & lt)] = ((uint32_t)e << 31) | (uint32_t)(py * fc.width + px);
   }
   if (kCount) {
+    // the method's count (SURVEY d-3, the oracle's orc_blend_pixel): the tile-list entries up to and
+    // including the one the pixel stopped before, the whole list if it never stopped
+    uint32_t nlist = !inside ? 0u : bias < 0.0f ? lstop - rg.x + 1 : rg.y > rg.x ? rg.y - rg.x : 0u;   // (empty tile: (~0, 0))
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
       nexp += __shfl_xor_sync(0xFFFFFFFFu, nexp, o);
+      nlist += __shfl_xor_sync(0xFFFFFFFFu, nlist, o);
     }
-    if (lane == 0 && nev) {
+    if (lane == 0 && nlist) {
       atomicAdd(&ctr->n_evals, (unsigned long long)nev);
       atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
+      atomicAdd(&ctr->n_evals_list, (unsigned long long)nlist);
     }
   }
   if (!inside || redo) return;
@@ -310,6 +320,7 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
   // per-warp slots: [0, 32) = spA, [32, 64) = spB, [64, 96) = (g, b, -, -); one address register
   // walks all three (offsets 0, 512, 1024 bytes)
   __shared__ float4 slots[kBWarps][96];
+  __shared__ uint32_t s_idx[kCount ? kBWarps * 32 : 1];   // (kCount) list index of each staged splat
   const int t = threadIdx.x;
   const uint32_t warp = (uint32_t)t >> 5, lane = lane_id();
   const int tile = blockIdx.x;
@@ -331,7 +342,7 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
   // outside the image), so nothing is live for it any more (one FMNMX instead of a predicate chain)
   const float kInf = __int_as_float(0x7F800000);
   float pfloor = inside ? -kInf : kInf;
-  uint32_t nev = 0, nexp = 0;
+  uint32_t nev = 0, nexp = 0, lstop = 0;
   uint32_t base = (uint32_t)__cvta_generic_to_shared(&slots[warp][0]);
   asm volatile("" : "+r"(base));   // keep the slot address in a register
   const uint32_t lt = lanemask_lt();
@@ -347,6 +358,7 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
     if (in) {
       const uint32_t c = pair_vals[idx];
       const uint32_t slot = __popc(bits & lt);
+      if (kCount) s_idx[warp * 32 + slot] = idx;
       slots[warp][slot] = spA[c];
       slots[warp][32 + slot] = spB[c];
       *reinterpret_cast<float2 *>(&slots[warp][64 + slot]) = spC[c];
@@ -371,7 +383,10 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
       al = (live && al >= kAlphaMin) ? al : 0.0f;
       const float Tn = __fmaf_rn(-al, T, T);
       const bool term = Tn < 0.0001f;   // terminate before this splat; the rest is not evaluated
-      if (kCount && term) pstop = p;
+      if (kCount && term) {
+        pstop = p;
+        lstop = s_idx[warp * 32 + j];
+      }
       if (!term) {
         const float w = __fmul_rn(al, T);
         const float2 gb = lds_f2(p + 1024);
@@ -387,14 +402,17 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
     __syncwarp();
   }
   if (kCount) {
+    uint32_t nlist = !inside ? 0u : pfloor > 0.0f ? lstop - rg.x + 1 : rg.y > rg.x ? rg.y - rg.x : 0u;   // (as blend_kernel)
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       nev += __shfl_xor_sync(0xFFFFFFFFu, nev, o);
       nexp += __shfl_xor_sync(0xFFFFFFFFu, nexp, o);
+      nlist += __shfl_xor_sync(0xFFFFFFFFu, nlist, o);
     }
-    if (lane == 0 && nev) {
+    if (lane == 0 && nlist) {
       atomicAdd(&ctr->n_evals, (unsigned long long)nev);
       atomicAdd(&ctr->n_exp, (unsigned long long)nexp);
+      atomicAdd(&ctr->n_evals_list, (unsigned long long)nlist);
     }
   }
   if (!inside) return;

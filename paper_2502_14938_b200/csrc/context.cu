@@ -676,6 +676,7 @@ static void fill_stats(gsc_ctx *ctx, int64_t frame_seq, gsc_frame_stats *s) {
   s->overflow = r.overflow;
   s->n_evals = r.n_evals;
   s->n_exp = r.n_exp;
+  s->n_evals_list = r.n_evals_list;
   s->n_nonfinite_skipped = r.n_nonfinite;
   s->n_blend_fixup = r.n_fixup;
   s->depth_used = r.depth_used;

@@ -241,6 +241,7 @@ __global__ void record_kernel(const FrameCounters *ctr, FrameRecordDev *rec) {
   rec->n_fixup = ctr->n_fixup;
   rec->n_evals = ctr->n_evals;
   rec->n_exp = ctr->n_exp;
+  rec->n_evals_list = ctr->n_evals_list;
 }
 
 // load-time: m_i = max_j |O_ij (.) s_i|_2 + 3.33 max_k s_ik  (R8), packed with pos

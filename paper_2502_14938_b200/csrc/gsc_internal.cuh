@@ -49,6 +49,7 @@ struct FrameCounters {
   uint32_t list_top;           // project: bump allocator of the kept-tile list
   unsigned long long n_evals;  // blend: (pixel, splat) evaluations executed
   unsigned long long n_exp;    // blend: evaluations that reached exp_s
+  unsigned long long n_evals_list;   // blend: the method's evaluations (tile-list entries up to each pixel's stop)
   uint32_t tile_pairoff, tile_expand;
   uint32_t list_overflow;      // project: the kept-tile list ran out (the frame's pairs are dropped)
   uint32_t n_nonfinite;        // project: (Gaussian, eye) skipped for non-finite parameters
@@ -100,7 +101,7 @@ struct EmitIn {
 struct FrameRecordDev {
   int32_t frame, depth_used, depth_next, pad0;
   uint32_t n_visible, n_miss, n_new, n_splat, n_pairs_raw, overflow, n_nonfinite, n_fixup;
-  unsigned long long n_evals, n_exp;
+  unsigned long long n_evals, n_exp, n_evals_list;
 };
 
 // Launch configuration kept per CUDA device (grid sizes from the device's occupancy, the

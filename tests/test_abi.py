@@ -37,7 +37,7 @@ def test_every_declared_symbol_is_exported(gsclib):
 
 def test_abi_version_and_argument_checks(gsclib):
     L = gsclib.lib()
-    assert L.gsc_abi_version() == 3
+    assert L.gsc_abi_version() == 4
     h = C.c_void_p()
     cfg = gsclib.gsc_config()
     assert L.gsc_create(0, C.byref(cfg), C.byref(h)) == gsclib.GSC_EINVAL      # zero-sized image

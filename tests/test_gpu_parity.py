@@ -277,6 +277,29 @@ def test_c3_trajectory_reuse(orc, c100k):
     assert hits > 0
 
 
+def test_eval_counts_match_oracle(orc, c1, c100k):
+    """The blend's evaluation count for the roofline (gsc_frame_stats.n_evals_list, GSC_F_COUNT_EVALS): per
+    pixel, the tile-list entries up to and including the splat it stops before -- the oracle's own
+    orc_blend_pixel count (SURVEY d-3).  The exact-exponential kernel reproduces it exactly; the default
+    kernel within 1e-3 (a pixel the fast path flags for the exact replay may stop one splat apart).  The
+    executed count (after the 8x4-block skip) never exceeds it."""
+    import paper_2502_14938_b200 as gp
+    for cfg, sc, frames in ((c1[0], c1[1], range(4)), (c100k[0], c100k[1], (0, 1, 150))):
+        traj = sg.trajectory(cfg)
+        for flags, tol in ((gp.GSC_F_COUNT_EVALS | gp.GSC_F_BLEND_EXACT, 0.0), (gp.GSC_F_COUNT_EVALS, 1e-3)):
+            o = orc.Oracle(sc, oracle_config(orc, cfg))
+            r = renderer(cfg, flags=flags).load(sc)
+            for f in range(max(frames) + 1):
+                res = o.frame(traj[f], raster=f in frames, images=f in frames)
+                _, _, st = r.render(traj[f])
+                if f not in frames:
+                    continue
+                ref = res.stats.n_evals
+                assert ref > 0
+                assert abs(int(st["n_evals_list"]) - ref) <= tol * ref, (cfg.name, f, flags, st["n_evals_list"], ref)
+                assert 0 < st["n_evals"] <= st["n_evals_list"]
+
+
 # ---------------------------------------------------------------- configs[3] at full size (bench launch config)
 @pytest.fixture(scope="module")
 def c4():
