@@ -78,22 +78,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
 constexpr int kBWarps = kBThreads / 32;
 
 
-// Packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2: two IEEE fp32 operations per instruction, each
-// element rounded exactly as the scalar __fadd_rn / __fmul_rn / __fmaf_rn; a scalar operand is broadcast
-// by the hardware, so a splat-pair or pixel constant costs no move).
-struct f2p { unsigned long long r; };
-__device__ __forceinline__ f2p pk2(float a, float b) {
-  f2p o; asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b)); return o;
-}
-__device__ __forceinline__ void up2(f2p x, float &a, float &b) {
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.r));
-}
-__device__ __forceinline__ f2p add2(f2p a, f2p b) { f2p o; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
-__device__ __forceinline__ f2p mul2(f2p a, f2p b) { f2p o; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
-__device__ __forceinline__ f2p fma2(f2p a, f2p b, f2p c) {
-  f2p o; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r)); return o;
-}
-__device__ __forceinline__ f2p bc2(float a) { return pk2(a, a); }
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d; asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c)); return d;
 }

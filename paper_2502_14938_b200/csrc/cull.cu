@@ -25,15 +25,29 @@ constexpr int kCullThreads = 512;
 constexpr int kCullItems = 8;                                  // per thread
 constexpr int kCullTile = kCullThreads * kCullItems;           // 4096 anchors
 
-__device__ __forceinline__ bool cull_visible(const UniC &u, float4 pm, int level, int L, float d0) {
-  float v0 = __fsub_rn(pm.x, u.p[0]), v1 = __fsub_rn(pm.y, u.p[1]), v2 = __fsub_rn(pm.z, u.p[2]);
-  float x = dot3(v0, v1, v2, u.right), y = dot3(v0, v1, v2, u.up), z = dot3(v0, v1, v2, u.fwd);
+// (x, y) = (dot3(v, right), dot3(v, up)): the products as packed pairs (v_k broadcast, rp_k = (right_k,
+// up_k)), the sums as scalar IEEE adds in dot3's order ((v0 b0 + v1 b1) + v2 b2).  Not add.rn.f32x2:
+// ptxas fuses mul.rn.f32x2 -> add.rn.f32x2 into FFMA2 even under --fmad=false (checked in SASS), which
+// would change the rounding; a scalar add.rn after a packed multiply is left alone.
+__device__ __forceinline__ bool cull_visible(const UniC &u, f2p rp0, f2p rp1, f2p rp2, float4 pm, int level, int L,
+                                             float d0) {
+  float v0, v1;
+  up2(add2(pk2(pm.x, pm.y), pk2(-u.p[0], -u.p[1])), v0, v1);   // fl(pm - p): adding -p is subtracting
+  const float v2 = __fsub_rn(pm.z, u.p[2]);
+  float p0x, p0y, p1x, p1y, p2x, p2y;
+  up2(mul2(bc2(v0), rp0), p0x, p0y);
+  up2(mul2(bc2(v1), rp1), p1x, p1y);
+  up2(mul2(bc2(v2), rp2), p2x, p2y);
+  const float x = __fadd_rn(__fadd_rn(p0x, p1x), p2x), y = __fadd_rn(__fadd_rn(p0y, p1y), p2y);
+  const float z = dot3(v0, v1, v2, u.fwd);
   float m = pm.w;
   bool fr = (z >= __fsub_rn(u.near_plane, m)) && (z <= __fadd_rn(u.far_plane, m)) &&
             (__fsub_rn(fabsf(x), __fmul_rn(u.tx, z)) <= __fmul_rn(m, u.kx)) &&
             (__fsub_rn(fabsf(y), __fmul_rn(u.ty, z)) <= __fmul_rn(m, u.ky));
   if (!fr) return false;
-  float d2 = __fadd_rn(__fadd_rn(__fmul_rn(v0, v0), __fmul_rn(v1, v1)), __fmul_rn(v2, v2));
+  float s0, s1;
+  up2(mul2(pk2(v0, v1), pk2(v0, v1)), s0, s1);
+  float d2 = __fadd_rn(__fadd_rn(s0, s1), __fmul_rn(v2, v2));
   int lc;
   if (d2 == 0.0f) {
     lc = L - 1;
@@ -45,18 +59,19 @@ __device__ __forceinline__ bool cull_visible(const UniC &u, float4 pm, int level
     int e;
     const uint32_t yb = __float_as_uint(__fmul_rn(d0, rsqrtf(d2)));
     const uint32_t ym = yb & 0x7FFFFFu, yx = yb >> 23;
-    if (d2 >= 1e-30f && d2 <= 1e30f && ym > 256u && ym < 0x7FFFFFu - 256u && yx - 1u < 253u)
+    if (d2 >= 1e-30f && d2 <= 1e30f && ym - 257u < 0x7FFFFFu - 513u && yx - 1u < 253u)
       e = (int)yx - 127;
     else
       e = ilogb_bits(__fdiv_rn(d0, __fsqrt_rn(d2)));
-    long long l = (long long)e + (L - 1);
-    lc = (int)(l < 0 ? 0 : (l > L - 1 ? L - 1 : l));
+    // e in [-149, 127] or INT_MAX (inf / nan): clamp before the add (int arithmetic, no overflow)
+    const int l = min(max(e, -1000), 1000) + (L - 1);
+    lc = l < 0 ? 0 : (l > L - 1 ? L - 1 : l);
   }
   return level <= lc;
 }
 
 // Pass 1 (independent tiles): predicates, cache classify, birth update, the frame's visibility and
-// miss bitsets, per-tile (visible, miss) counts -> agg[tile].
+// miss bitsets, per-tile (visible, miss) counts -> agg[tile].  N < 2^31: 32-bit indices.
 __global__ void __launch_bounds__(kCullThreads)
 cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ pos_m,
                      const uint8_t *__restrict__ level, int32_t *__restrict__ birth,
@@ -67,7 +82,8 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
   const uint32_t warp = threadIdx.x >> 5, lane = lane_id();
   const uint32_t tile = blockIdx.x;
   const int32_t f = pol->frame, W = pol->W;
-  const int64_t wbase = (int64_t)tile * kCullTile + warp * (32 * kCullItems);
+  const uint32_t n = (uint32_t)N;
+  const uint32_t wbase = tile * kCullTile + warp * (32 * kCullItems);
 
   // all of the thread's anchor loads in flight before the first predicate (and the previous frame's
   // visibility words of the warp's 8 groups: lane k holds group k's)
@@ -75,25 +91,26 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
   int lv[kCullItems];
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
-    const int64_t i = wbase + it * 32 + lane;
-    pm[it] = i < N ? pos_m[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    lv[it] = i < N ? level[i] : 0;
+    const uint32_t i = wbase + it * 32 + lane;
+    pm[it] = i < n ? pos_m[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    lv[it] = i < n ? level[i] : 0;
   }
   const uint32_t pw_lane =
-      (lane < (uint32_t)kCullItems && wbase + lane * 32 < N) ? prev_vis[(wbase >> 5) + lane] : 0u;
+      (lane < (uint32_t)kCullItems && wbase + lane * 32 < n) ? prev_vis[(wbase >> 5) + lane] : 0u;
+  const f2p rp0 = pk2(u.right[0], u.up[0]), rp1 = pk2(u.right[1], u.up[1]), rp2 = pk2(u.right[2], u.up[2]);
   // predicates first; the cache lines (birth) are read for the visible anchors only, all in flight
   bool vis[kCullItems];
   int32_t bi[kCullItems];
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
-    const int64_t i = wbase + it * 32 + lane;
-    vis[it] = i < N && cull_visible(u, pm[it], lv[it], L, d0);
+    const uint32_t i = wbase + it * 32 + lane;
+    vis[it] = i < n && cull_visible(u, rp0, rp1, rp2, pm[it], lv[it], L, d0);
     bi[it] = vis[it] ? birth[i] : 0;
   }
   uint32_t cnt_v = 0, cnt_m = 0, cnt_new = 0;
 #pragma unroll
   for (int it = 0; it < kCullItems; ++it) {
-    const int64_t i = wbase + it * 32 + lane;
+    const uint32_t i = wbase + it * 32 + lane;
     bool miss = false;
     if (vis[it]) {
       {
@@ -112,9 +129,9 @@ cull_classify_kernel(UniC u, int L, float d0, int N, const float4 *__restrict__ 
     }
     const uint32_t mv = __ballot_sync(0xFFFFFFFFu, vis[it]);
     const uint32_t mm = __ballot_sync(0xFFFFFFFFu, miss);
-    const int64_t word = (wbase + it * 32) >> 5;
+    const uint32_t word = (wbase + it * 32) >> 5;
     const uint32_t pw = __shfl_sync(0xFFFFFFFFu, pw_lane, it);
-    if (wbase + it * 32 < N) {
+    if (wbase + it * 32 < n) {
       if (lane == 0) { cur_vis[word] = mv; miss_bits[word] = mm; }
       cnt_new += __popc(mv & ~pw);
     }

@@ -381,6 +381,22 @@ __device__ __forceinline__ float sigmoid_s(float x) {
   return __fdiv_rn(1.0f, __fadd_rn(1.0f, exp_s(-x)));
 }
 
+// Packed fp32x2 helpers (sm_100a FADD2 / FMUL2 / FFMA2: two IEEE fp32 operations per instruction, each
+// element rounded exactly as the scalar __fadd_rn / __fmul_rn / __fmaf_rn; a scalar operand is broadcast
+// by the hardware, so a splat-pair or pixel constant costs no move).
+struct f2p { unsigned long long r; };
+__device__ __forceinline__ f2p pk2(float a, float b) {
+  f2p o; asm("mov.b64 %0, {%1, %2};" : "=l"(o.r) : "f"(a), "f"(b)); return o;
+}
+__device__ __forceinline__ void up2(f2p x, float &a, float &b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(x.r));
+}
+__device__ __forceinline__ f2p add2(f2p a, f2p b) { f2p o; asm("add.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
+__device__ __forceinline__ f2p mul2(f2p a, f2p b) { f2p o; asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(o.r) : "l"(a.r), "l"(b.r)); return o; }
+__device__ __forceinline__ f2p fma2(f2p a, f2p b, f2p c) {
+  f2p o; asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(o.r) : "l"(a.r), "l"(b.r), "l"(c.r)); return o;
+}
+__device__ __forceinline__ f2p bc2(float a) { return pk2(a, a); }
 // exact dot product in the written order ((a0 b0 + a1 b1) + a2 b2)
 __device__ __forceinline__ float dot3(float a0, float a1, float a2, const float *b) {
   return __fadd_rn(__fadd_rn(__fmul_rn(a0, b[0]), __fmul_rn(a1, b[1])), __fmul_rn(a2, b[2]));

@@ -21,6 +21,9 @@ sys.path.insert(0, ROOT)
 
 
 def main(n=18_000_000, frames=60, out=None):
+    if os.environ.get("GSC_AB_LIB"):   # A/B measurement of a variant build (tools/ab_build.py)
+        from paper_2502_14938_b200 import _abi
+        _abi.SO_PATH = os.environ["GSC_AB_LIB"]
     import torch
     import scenegen as sg
     import paper_2502_14938_b200 as gp
