@@ -150,17 +150,26 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(stage + warp * kWarpStage);
   const uint32_t lt = lanemask_lt();
 
+  // the pair keys run two chunks ahead and the block's splat ids one chunk ahead (registers), so a
+  // chunk's staging waits only on its records, not on the key -> id -> record chain
+  const uint32_t wbit = 24 + warp;
+  uint32_t key0 = rg.x + lane < rg.y ? pair_keys[rg.x + lane] : 0u;
+  uint32_t key1 = rg.x + 32 + lane < rg.y ? pair_keys[rg.x + 32 + lane] : 0u;
+  uint32_t val0 = ((key0 >> wbit) & 1u) ? pair_vals[rg.x + lane] : 0u;
   for (uint32_t b = rg.x; b < rg.y; b += 32) {
     if (__all_sync(0xFFFFFFFFu, bias < 0.0f)) break;
     const uint32_t idx = b + lane;
     // the pair key's block mask (bit = warp) says whether the splat's box of {power >= skip bound}
     // meets this warp's 8x4 block (computed by project.cu with the fp32 test of DESIGN.md N5)
-    const bool in = idx < rg.y && ((pair_keys[idx] >> (24 + warp)) & 1u);
+    const bool in = (key0 >> wbit) & 1u;   // (key0 = 0 past the end)
+    const uint32_t c = val0;
+    val0 = ((key1 >> wbit) & 1u) ? pair_vals[idx + 32] : 0u;
+    key0 = key1;
+    key1 = idx + 64 < rg.y ? pair_keys[idx + 64] : 0u;
     // compact the block's splats into the warp's pair-group planes, depth order preserved
     const uint32_t bits = __ballot_sync(0xFFFFFFFFu, in);
     const uint32_t n = __popc(bits);
     if (in) {
-      const uint32_t c = pair_vals[idx];
       const uint32_t slot = __popc(bits & lt);
       if (kCount) s_idx[warp * 32 + slot] = idx;
       const float4 A = spA[c], B = spB[c];
