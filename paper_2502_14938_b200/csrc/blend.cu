@@ -171,6 +171,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     const uint32_t n = __popc(bits);
     if (in) {
       const uint32_t slot = __popc(bits & lt);
+      GSC_CHECK(slot < 32u && idx < ctr->n_pairs && c < ctr->n_splat);
       if (kCount) s_idx[warp * 32 + slot] = idx;
       const float4 A = spA[c], B = spB[c];
       const float2 Cc = spC[c];
@@ -278,6 +279,7 @@ blend_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__rest
     uint32_t at = 0;
     if (lane == 0) at = atomicAdd(&ctr->n_fixup, (uint32_t)__popc(rb));
     at = __shfl_sync(0xFFFFFFFFu, at, 0);
+    GSC_CHECK(!redo || at + __popc(rb & lt) < 2u * (uint32_t)(fc.width * fc.height));
     if (redo) fixup[at + __popc(rb & lt)] = ((uint32_t)e << 31) | (uint32_t)(py * fc.width + px);
   }
   if (kCount) {
@@ -444,6 +446,7 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
       float al = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
       if (i < r1 && (pair_keys[i] & wbit)) {
         const uint32_t c = pair_vals[i];
+        GSC_CHECK(i < ctr->n_pairs && c < ctr->n_splat);
         const float4 a = spA[c], q = spB[c];
         const float2 cc = spC[c];
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);

@@ -178,6 +178,7 @@ expand_kernel(EmitIn in, uint32_t *__restrict__ keys_out, uint32_t *__restrict__
         const uint32_t oc = __shfl_sync(0xFFFFFFFFu, c, l), ol = __shfl_sync(0xFFFFFFFFu, lo, l),
                        oo = __shfl_sync(0xFFFFFFFFu, off, l);
         if (q < ge) {
+          GSC_CHECK(q < P && q >= oo && oc < C);
           const uint32_t key = in.list[ol + (q - oo)];
           keys_out[q] = key;
           vals_out[q] = oc;

@@ -4,6 +4,7 @@
 // -ftz=false so IEEE fp32 ops are emitted exactly as written (FMA only where
 // __fmaf_rn is spelled out).
 #pragma once
+#include <cstdio>
 #include <cstdint>
 #include <mutex>
 #include <cuda_runtime.h>
@@ -37,6 +38,23 @@ struct FrameC {
 constexpr int kAblFixedExtent = 1;
 constexpr int kAblAabbTiles = 2;
 constexpr int kAblMono = 4;       // GSC_F_MONO: left eye only (per-eye pipelines of the no-de-redundancy ablation)
+
+// GSC_BOUNDS_CHECK (a debug build, tools/bounds_build.py): device-side checks of the data-dependent
+// indices (staging slots, record / pair / list / output positions) that trap with a message when one is
+// out of range -- the stand-in for compute-sanitizer memcheck where the pool does not offer it.  A
+// no-op in the product build.
+#ifdef GSC_BOUNDS_CHECK
+#define GSC_CHECK(c)                                                                         \
+  do {                                                                                       \
+    if (!(c)) {                                                                              \
+      printf("GSC_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, #c,    \
+             (int)blockIdx.x, (int)threadIdx.x);                                             \
+      __trap();                                                                              \
+    }                                                                                        \
+  } while (0)
+#else
+#define GSC_CHECK(c) do { } while (0)
+#endif
 
 // ---- device-resident counters, zeroed at every frame start ----
 struct FrameCounters {

@@ -180,6 +180,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
       if (idx < n) {
         uint32_t d = (key[i] >> shift) & dmask;
         uint32_t pos = S.whist[warp][d] + rank[i];
+        GSC_CHECK(pos < (uint32_t)kSTile);
         S.kv[pos] = make_uint2(key[i], kIota ? idx : vals_in[idx]);
       }
     }
@@ -190,6 +191,7 @@ onesweep_pass_kernel(const uint32_t *__restrict__ keys_in, const uint32_t *__res
       const uint32_t k = e.x;
       uint32_t d = (k >> shift) & dmask;
       uint32_t o = S.gbase[d] + i;
+      GSC_CHECK(o < n);
       keys_out[o] = k;
       vals_out[o] = e.y;
       if (kRanges) {
