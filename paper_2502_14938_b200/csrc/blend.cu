@@ -440,15 +440,33 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
     const uint32_t r0 = ~ranges[tile].x, r1 = ranges[tile].y;
     float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
     bool stop = false;
+    // software pipeline over the chunks (the walk is latency-bound: one warp per pixel): keys three
+    // chunks ahead, splat ids two, records one
+    auto key_at = [&](uint32_t i) -> uint32_t { return i < r1 ? pair_keys[i] : 0u; };
+    uint32_t k0 = key_at(r0 + lane), k1 = key_at(r0 + 32 + lane), k2 = key_at(r0 + 64 + lane);
+    uint32_t v1 = (k1 & wbit) ? pair_vals[r0 + 32 + lane] : 0u;
+    float4 nA = make_float4(0.f, 0.f, 0.f, 0.f), nB = nA;
+    float2 nC = make_float2(0.f, 0.f);
+    if (k0 & wbit) {
+      const uint32_t c = pair_vals[r0 + lane];
+      GSC_CHECK(r0 + lane < ctr->n_pairs && c < ctr->n_splat);
+      nA = spA[c]; nB = spB[c]; nC = spC[c];
+    }
     for (uint32_t b = r0; b < r1 && !stop; b += 32) {
-      const uint32_t i = b + lane;
+      const bool has = k0 & wbit;   // (k0 = 0 past the end)
+      const float4 a = nA, q = nB;
+      const float2 cc = nC;
+      if (k1 & wbit) {
+        GSC_CHECK(b + 32 + lane < ctr->n_pairs && v1 < ctr->n_splat);
+        nA = spA[v1]; nB = spB[v1]; nC = spC[v1];
+      }
+      v1 = (k2 & wbit) ? pair_vals[b + 64 + lane] : 0u;
+      k0 = k1;
+      k1 = k2;
+      k2 = key_at(b + 96 + lane);
       bool ok = false;
       float al = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
-      if (i < r1 && (pair_keys[i] & wbit)) {
-        const uint32_t c = pair_vals[i];
-        GSC_CHECK(i < ctr->n_pairs && c < ctr->n_splat);
-        const float4 a = spA[c], q = spB[c];
-        const float2 cc = spC[c];
+      if (has) {
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
         const float power = __fmaf_rn(dx, qq, __fmul_rn(__fmul_rn(q.x, dy), dy));
