@@ -416,20 +416,25 @@ blend_exact_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
 
 // Exact replay of the flagged pixels: the oracle's per-pixel loop (O-8, N6) with exp_s over
 // the tile's sorted list (the pair key's block bit skips splats whose skip box misses the pixel's 8x4
-// block: decision-preserving, N5).  One warp per pixel: the lanes take 32 consecutive pairs, evaluate
-// power / alpha' / the skip decisions exactly and in parallel, then the accepted ones are composited in
-// order (the T chain is sequential: one shuffle round per accepted splat).
-__global__ void __launch_bounds__(128)
+// block: decision-preserving, N5).  One CTA of 8 warps per pixel: a window of 256 consecutive pairs is
+// evaluated in parallel (warp w takes the window's chunk w: power / alpha' / the skip decisions exactly,
+// the accepted ones compacted in order into the warp's SMEM row), then warp 0 composites the window's
+// accepted splats in list order (the T chain is sequential).  Keys run three windows ahead, splat ids
+// two, records one (registers), so a window waits on none of its own loads.
+constexpr int kFixThreads = 256;
+__global__ void __launch_bounds__(kFixThreads)
 blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *__restrict__ pair_keys,
                    const uint32_t *__restrict__ pair_vals, const float4 *__restrict__ spA,
                    const float4 *__restrict__ spB, const float2 *__restrict__ spC, void *__restrict__ out_l,
                    void *__restrict__ out_r, int fmt, const FrameCounters *__restrict__ ctr,
                    const uint32_t *__restrict__ fixup) {
-  const uint32_t lane = lane_id();
-  const uint32_t nfix = __shfl_sync(0xFFFFFFFFu, ctr->n_fixup, 0);
-  const uint32_t gw = __shfl_sync(0xFFFFFFFFu, (blockIdx.x * blockDim.x + threadIdx.x) >> 5, 0);
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t k = gw; k < nfix; k += nw) {
+  constexpr int kW = kFixThreads / 32;
+  __shared__ float4 s_acc[kW][32];   // accepted (alpha', r, g, b) of each chunk of the window, list order
+  __shared__ uint32_t s_n[kW];
+  __shared__ int s_stop;
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5, lt = lanemask_lt();
+  const uint32_t nfix = ctr->n_fixup;
+  for (uint32_t k = blockIdx.x; k < nfix; k += gridDim.x) {
     const uint32_t code = fixup[k];
     const int e = (int)(code >> 31);
     const int pix = (int)(code & 0x7FFFFFFFu);
@@ -438,34 +443,32 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
     const uint32_t wbit = 1u << (24 + ((px % kTile) >> 3) + 2 * ((py % kTile) >> 2));
     const float pxc = __fadd_rn((float)px, 0.5f), pyc = __fadd_rn((float)py, 0.5f);
     const uint32_t r0 = ~ranges[tile].x, r1 = ranges[tile].y;
-    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;
-    bool stop = false;
-    // software pipeline over the chunks (the walk is latency-bound: one warp per pixel): keys three
-    // chunks ahead, splat ids two, records one
+    float T = 1.0f, C0 = 0.0f, C1 = 0.0f, C2 = 0.0f;   // (warp 0)
     auto key_at = [&](uint32_t i) -> uint32_t { return i < r1 ? pair_keys[i] : 0u; };
-    uint32_t k0 = key_at(r0 + lane), k1 = key_at(r0 + 32 + lane), k2 = key_at(r0 + 64 + lane);
-    uint32_t v1 = (k1 & wbit) ? pair_vals[r0 + 32 + lane] : 0u;
+    const uint32_t t = threadIdx.x;
+    uint32_t k0 = key_at(r0 + t), k1 = key_at(r0 + kFixThreads + t), k2 = key_at(r0 + 2 * kFixThreads + t);
+    uint32_t v1 = (k1 & wbit) ? pair_vals[r0 + kFixThreads + t] : 0u;
     float4 nA = make_float4(0.f, 0.f, 0.f, 0.f), nB = nA;
     float2 nC = make_float2(0.f, 0.f);
     if (k0 & wbit) {
-      const uint32_t c = pair_vals[r0 + lane];
-      GSC_CHECK(r0 + lane < ctr->n_pairs && c < ctr->n_splat);
+      const uint32_t c = pair_vals[r0 + t];
+      GSC_CHECK(r0 + t < ctr->n_pairs && c < ctr->n_splat);
       nA = spA[c]; nB = spB[c]; nC = spC[c];
     }
-    for (uint32_t b = r0; b < r1 && !stop; b += 32) {
+    for (uint32_t wb = r0; wb < r1; wb += kFixThreads) {   // CTA-uniform
       const bool has = k0 & wbit;   // (k0 = 0 past the end)
       const float4 a = nA, q = nB;
       const float2 cc = nC;
       if (k1 & wbit) {
-        GSC_CHECK(b + 32 + lane < ctr->n_pairs && v1 < ctr->n_splat);
+        GSC_CHECK(wb + kFixThreads + t < ctr->n_pairs && v1 < ctr->n_splat);
         nA = spA[v1]; nB = spB[v1]; nC = spC[v1];
       }
-      v1 = (k2 & wbit) ? pair_vals[b + 64 + lane] : 0u;
+      v1 = (k2 & wbit) ? pair_vals[wb + 2 * kFixThreads + t] : 0u;
       k0 = k1;
       k1 = k2;
-      k2 = key_at(b + 96 + lane);
+      k2 = key_at(wb + 3 * kFixThreads + t);
       bool ok = false;
-      float al = 0.0f, cr = 0.0f, cg = 0.0f, cb = 0.0f;
+      float al = 0.0f;
       if (has) {
         const float dx = __fsub_rn(a.x, pxc), dy = __fsub_rn(a.y, pyc);
         const float qq = __fmaf_rn(a.z, dx, __fmul_rn(a.w, dy));
@@ -473,24 +476,34 @@ blend_fixup_kernel(FrameC fc, const uint2 *__restrict__ ranges, const uint32_t *
         if (!(power > 0.0f)) {
           al = fminf(0.99f, __fmul_rn(q.z, exp_s(power)));
           ok = al >= kAlphaMin;
-          cr = q.w; cg = cc.x; cb = cc.y;
         }
       }
-      uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
-      while (m) {   // warp-uniform
-        const int l = __ffs(m) - 1;
-        m &= m - 1;
-        const float a = __shfl_sync(0xFFFFFFFFu, al, l);
-        const float Tn = __fmaf_rn(-a, T, T);
-        if (Tn < 0.0001f) { stop = true; break; }
-        const float w = __fmul_rn(a, T);
-        C0 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cr, l), w, C0);
-        C1 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cg, l), w, C1);
-        C2 = __fmaf_rn(__shfl_sync(0xFFFFFFFFu, cb, l), w, C2);
-        T = Tn;
+      const uint32_t m = __ballot_sync(0xFFFFFFFFu, ok);
+      if (ok) s_acc[warp][__popc(m & lt)] = make_float4(al, q.w, cc.x, cc.y);
+      if (lane == 0) s_n[warp] = __popc(m);
+      __syncthreads();
+      if (warp == 0) {
+        bool stop = false;
+        for (uint32_t w = 0; w < (uint32_t)kW && !stop; ++w) {
+          const uint32_t n = s_n[w];
+          for (uint32_t j = 0; j < n; ++j) {   // warp-uniform (broadcast reads)
+            const float4 r = s_acc[w][j];
+            const float Tn = __fmaf_rn(-r.x, T, T);
+            if (Tn < 0.0001f) { stop = true; break; }
+            const float wgt = __fmul_rn(r.x, T);
+            C0 = __fmaf_rn(r.y, wgt, C0);
+            C1 = __fmaf_rn(r.z, wgt, C1);
+            C2 = __fmaf_rn(r.w, wgt, C2);
+            T = Tn;
+          }
+        }
+        if (lane == 0) s_stop = stop;
       }
+      __syncthreads();
+      if (s_stop) break;
     }
-    if (lane == 0) write_pixel(fc, e, px, py, T, C0, C1, C2, out_l, out_r, fmt);
+    if (t == 0) write_pixel(fc, e, px, py, T, C0, C1, C2, out_l, out_r, fmt);
+    __syncthreads();   // (s_acc / s_n / s_stop reuse by the next pixel)
   }
 }
 
@@ -513,7 +526,7 @@ void launch_blend(const FrameC &fc, const uint2 *ranges, const uint32_t *pair_ke
   else
     blend_kernel<false><<<grid, kBThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt,
                                                     ctr, fixup);
-  blend_fixup_kernel<<<4 * num_sms, 128, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr,
+  blend_fixup_kernel<<<4 * num_sms, kFixThreads, 0, st>>>(fc, ranges, pair_keys, pair_vals, spA, spB, spC, out_l, out_r, fmt, ctr,
                                                   fixup);
 }
 
