@@ -54,8 +54,14 @@ pairoff_reduce_kernel(EmitIn in, uint32_t *__restrict__ agg, const FrameCounters
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     uint32_t cnt[kOffItems], sum = 0;
     pairoff_counts(in, C, tile, cnt);
+    // the gathered counts, in depth order, parked in pair_off (the scan reads them coalesced and
+    // overwrites them with the offsets)
+    const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;
 #pragma unroll
-    for (int i = 0; i < kOffItems; ++i) sum += cnt[i];
+    for (int i = 0; i < kOffItems; ++i) {
+      sum += cnt[i];
+      if (p0 + 32 * i < C) in.pair_off[p0 + 32 * i] = cnt[i];
+    }
     sum = __reduce_add_sync(0xFFFFFFFFu, sum);
     if (lane == 0) s_w[warp] = sum;
     __syncthreads();
@@ -80,7 +86,11 @@ pairoff_scan_kernel(EmitIn in, uint32_t cap, const uint32_t *__restrict__ agg, F
   const uint32_t ntiles = (C + kOffTile - 1) / kOffTile;
   for (uint32_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     uint32_t cnt[kOffItems], excl[kOffItems], run = 0;
-    pairoff_counts(in, C, tile, cnt);
+    {   // the counts pairoff_reduce parked in pair_off (coalesced: no second gather)
+      const uint32_t p0 = tile * kOffTile + warp * (32 * kOffItems) + lane;
+#pragma unroll
+      for (int i = 0; i < kOffItems; ++i) cnt[i] = p0 + 32 * i < C ? in.pair_off[p0 + 32 * i] : 0u;
+    }
     // prefix of the earlier tiles
     uint32_t pre = 0;
     for (uint32_t j = threadIdx.x; j < tile; j += kXThreads) pre += agg[j];
