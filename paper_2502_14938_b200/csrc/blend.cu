@@ -4,27 +4,29 @@
 // One 256-thread CTA per (eye, 16x16 tile); warp w owns the 8x4 pixel block
 // at columns 8 (w & 1) .., rows 4 (w >> 1) .., one pixel per lane, and runs
 // independently of the other warps (no block barrier): it walks the tile's
-// depth-sorted pair list in chunks of 32, keeps the splats whose padded
-// bounding box of {power >= skip bound} touches the block (one bit per block
-// in the pair key, computed by project.cu's tile walk), stages those records
-// in the warp's SMEM slots (the 8 warps of a CTA fetch overlapping records, so
-// most fetches are L1 hits),
-// evaluates them in depth order and leaves as soon as all 32 of its pixels
-// have terminated.  Skipping a (pixel, splat) by the box never changes a
-// decision: outside it power < -ln(255 alpha) - 2^-7, so alpha' < 1/255
-// (N5).  The evaluation loop is warp-uniform (no divergent
-// branches): a lane that skips a splat, or has terminated, composites it with
-// alpha' = 0, which leaves T and C bit-identical (fma(-0, T, T) = T,
-// fma(c, 0, C) = C); only when no lane of the warp needs the exp is the splat
-// skipped outright.
+// depth-sorted pair list in chunks of 32 (pair keys prefetched two chunks
+// ahead, the block's splat ids one), keeps the splats whose padded bounding
+// box of {power >= skip bound} touches the block (one bit per block in the
+// pair key, computed by project.cu's tile walk), stages those records in the
+// warp's SMEM planes as pair groups (the 8 warps of a CTA fetch overlapping
+// records, so most fetches are L1 hits), evaluates them two splats at a time
+// with packed fp32x2 instructions in depth order, and leaves as soon as all 32
+// of its pixels have terminated.  Skipping a (pixel, splat) by the box never
+// changes a decision: outside it power < -ln(255 alpha) - 2^-7, so alpha' <
+// 1/255 (N5).  The evaluation loop is warp-uniform: a lane that
+// skips a splat, or has terminated, composites it with alpha' = 0, which
+// leaves T and C bit-identical (fma(-0, T, T) = T, fma(c, 0, C) = C); the stop
+// bookkeeping runs on a warp-uniform slow path taken only when some lane's T'
+// nears the stop threshold.
 // Per evaluated (pixel, splat), the op order of DESIGN.md N6 (the oracle's), except the exponential:
 //   power  = fma(dx, fma(a', dx, b' dy), (c' dy) dy)      (skip if > 0)
 //   alpha' = min(0.99, alpha exp(power))                  (skip if < 1/255)
 //   T' = fma(-alpha', T, T); stop before T' < 1e-4; C = fma(c, alpha' T, C)
-// exp runs on the SFU (ex2.approx) with a guard band that takes the skip decision
-// with the exact exp_s where alpha' lies within 2^-16 relative of 1/255, so every skip decision is
-// the oracle's; pixels match it within ~1e-6 (<= 1e-4 where a T < 1e-4 stop flips), inside the
-// north_star tolerance (2e-3 per channel, PSNR >= 55 dB).
+// exp runs on the SFU (ex2.approx); a pixel where the fast exponential could have
+// flipped a skip or stop decision (alpha' within 2^-19 relative of 1/255, power > 0, T' within the
+// band around 1e-4) is replayed exactly by blend_fixup_kernel, so every decision is the oracle's;
+// pixels match it within ~1e-6 (<= 1e-4 where an unreplayed, immaterial stop flip remains), inside
+// the north_star tolerance (2e-3 per channel, PSNR >= 55 dB).
 #include "gsc_internal.cuh"
 
 namespace gsc {
