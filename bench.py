@@ -121,6 +121,9 @@ def run_gsc(args):
     import torch
     import scenegen as sg
     import paper_2502_14938_b200 as gp
+    if os.environ.get("GSC_AB_LIB"):   # A/B measurement of another build of the same sources (tools/ab_build.py)
+        from paper_2502_14938_b200 import _abi
+        _abi.SO_PATH = os.environ["GSC_AB_LIB"]
     from paper_2502_14938_b200 import multi
 
     # GSC_BENCH_SHARE_GPU=1: every rank on cuda:0 with a gloo process group -- exercises the
