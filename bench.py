@@ -376,9 +376,9 @@ def run_reference(args):
     sc = cfg.scene()
     traj = sg.trajectory(cfg)
     oc = oracle.make_config(cfg.width, cfg.height, cfg.fov_y_deg, cfg.near, cfg.far, cfg.d_max)
-    # one untimed warm-up frame (thread pool start-up, first touch of the scene), then a fresh oracle
-    # (cold cache, like the GPU arm's timed block) for the timed frames
-    nwarm = min(args.warmup, 1)
+    # W untimed warm-up frames (thread pool start-up, first touch of the scene; at most 5 to bound the
+    # run), then a fresh oracle (cold cache, like the GPU arm's timed block) for the timed frames
+    nwarm = min(args.warmup, 5)
     for f in range(nwarm):
         oracle.Oracle(sc, oc).frame(traj[f])
     o = oracle.Oracle(sc, oc)
@@ -422,7 +422,7 @@ def main():
     ap.add_argument("--gather", action="store_true", help="gather each frame's image to rank 0 (NCCL)")
     ap.add_argument("--blend-exact", action="store_true", help="blend with exp_s on every evaluation (GSC_F_BLEND_EXACT)")
     ap.add_argument("--cpu-sample-frames", type=int, default=1)
-    ap.add_argument("--ref-frames", type=int, default=4)
+    ap.add_argument("--ref-frames", type=int, default=20)
     args = ap.parse_args()
     if args.warmup < 3:
         print("warning: --warmup < 3 violates the timing rules", file=sys.stderr)
