@@ -60,3 +60,24 @@ def test_no_gpu_means_loud_failure(gsclib):
     cfg = gsclib.gsc_config()
     cfg.width, cfg.height, cfg.fov_y, cfg.near_plane, cfg.far_plane, cfg.d_max = 64, 64, 1.2, 0.05, 100.0, 10
     assert L.gsc_create(0, C.byref(cfg), C.byref(h)) == gsclib.GSC_ECUDA
+
+
+def test_bounds_checked_debug_build_compiles_its_checks(gsclib):
+    """tools/bounds_build.py (the stand-in for compute-sanitizer memcheck) still builds, its library
+    carries the GSC_CHECK trap sites, and the product library does not (the checks compile away)."""
+    import shutil
+    import subprocess
+    import sys
+    if not shutil.which("cuobjdump") and not os.path.exists("/usr/local/cuda/bin/cuobjdump"):
+        pytest.skip("no cuobjdump")
+    cuobjdump = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "bounds_build.py")], capture_output=True,
+                         text=True, check=True).stdout.strip().splitlines()[-1]
+    assert out.endswith("libgscache.so") and os.path.exists(out)
+
+    def traps(so):
+        sass = subprocess.run([cuobjdump, "-sass", so], capture_output=True, text=True, check=True).stdout
+        return sum(1 for line in sass.splitlines() if "TRAP" in line)
+
+    debug, product = traps(out), traps(gsclib.SO_PATH)
+    assert debug >= product + 40, (debug, product)
