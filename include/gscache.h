@@ -66,7 +66,8 @@ typedef struct gsc_ctx gsc_ctx;
 #define GSC_F_DEPTH_LITERAL 0x1u /* SPEC-literal H(miss rate) instead of H(novelty) */
 #define GSC_F_STAGE_TIMING 0x2u  /* record CUDA events between the stages of every frame */
 #define GSC_F_DERIVE_CUDA_CORES 0x4u /* derivation MLP on CUDA cores (dp4a) instead of tcgen05 tensor cores */
-#define GSC_F_COUNT_EVALS 0x8u   /* blend counts its evaluations (gsc_frame_stats.n_evals / n_exp; else 0);
+#define GSC_F_COUNT_EVALS 0x8u   /* blend counts its evaluations (gsc_frame_stats.n_evals / n_exp /
+                                    n_evals_list; else 0);
                                     costs blend time, so bench.py counts in a separate untimed pass */
 #define GSC_F_GUIDE_EXP 0x20u    /* guiding function H (Eq. 4): exponential response, depth = max(1, D_max >>
                                     floor(4 rate)) ("exponential response"; R23) */
