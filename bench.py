@@ -421,7 +421,7 @@ def main():
                     help="multi-GPU partition: frame blocks per rank, or one eye per rank (latency mode)")
     ap.add_argument("--gather", action="store_true", help="gather each frame's image to rank 0 (NCCL)")
     ap.add_argument("--blend-exact", action="store_true", help="blend with exp_s on every evaluation (GSC_F_BLEND_EXACT)")
-    ap.add_argument("--cpu-sample-frames", type=int, default=1)
+    ap.add_argument("--cpu-sample-frames", type=int, default=2)   # ~14 s of oracle work on 16 threads
     ap.add_argument("--ref-frames", type=int, default=20)
     args = ap.parse_args()
     if args.warmup < 3:
